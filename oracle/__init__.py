@@ -85,8 +85,17 @@ def sort_rows(rows: np.ndarray) -> np.ndarray:
     rows = np.ascontiguousarray(rows, dtype=np.int32)
     if rows.shape[0] <= 1:
         return rows
+    k = rows.shape[1]
     keys = rows.view(np.uint32)
-    order = np.lexsort(keys.T[::-1])
+    top = int(keys.max())
+    bits = max(1, top.bit_length())
+    if bits * k <= 64:  # one packed uint64 key per row (same order as the tuple order)
+        packed = np.zeros(rows.shape[0], dtype=np.uint64)
+        for j in range(k):
+            packed = (packed << np.uint64(bits)) | keys[:, j].astype(np.uint64)
+        order = np.argsort(packed, kind="stable")
+    else:
+        order = np.lexsort(keys.T[::-1])
     return rows[order]
 
 

@@ -1,0 +1,382 @@
+// gsm_graph.cu — gsm_load_graph / gsm_free: the device replica of the data graph.
+//
+// PAPER P:148 (§3.3): "We store graphs in a space-efficient fashion on the GPU
+// by using compressed sparse row (CSR)".  P:47: the method inputs CSR and does
+// no index building on G.  We add one O(m log m) relabelling at load time
+// (reported as load time, never inside gsm_match): vertices are
+// renumbered by ascending (degree, original id) and every list is re-sorted.
+// After it, the symmetry-breaking total order ≺ on data vertices (P:71
+// constraints) is plain integer '<' on new ids, and
+// N+(v) = {w in N(v) : v ≺ w} is the contiguous suffix of v's sorted list
+// starting at up[v].  Every id crossing the ABI is an original id.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cstring>
+#include <memory>
+#include <new>
+
+#include "gsm_common.h"
+
+struct gsm_graph {
+    gsm::DevGraph g;
+    int device = 0;
+    cudaStream_t stream = 0;
+    bool own_stream = false;
+    bool labeled = false;
+};
+
+namespace gsm {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+void clear_error() { g_last_error.clear(); }
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+        fail(e == cudaErrorMemoryAllocation ? GSM_ERR_OUT_OF_MEMORY : GSM_ERR_CUDA, buf);
+    }
+    return p;
+}
+
+void dev_free(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+// ---------------------------------------------------------------- validation kernels
+__global__ void k_validate_offsets(const int64_t* __restrict__ off, int64_t n, int64_t nnz, int* err) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        if (off[v] > off[v + 1]) atomicOr(err, 1);
+        if (v == 0 && off[0] != 0) atomicOr(err, 1);
+        if (v == n - 1 && off[n] != nnz) atomicOr(err, 1);
+    }
+}
+
+// warp per vertex: ids in range, no self-loop, strictly ascending, symmetric
+__global__ void k_validate_lists(const int64_t* __restrict__ off, const int32_t* __restrict__ cols, int64_t n,
+                                 int* err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = warp; u < n; u += nwarps) {
+        const int64_t b = off[u], e = off[u + 1];
+        for (int64_t i = b + lane; i < e; i += 32) {
+            const int32_t c = cols[i];
+            if (c < 0 || c >= n) { atomicOr(err, 2); continue; }
+            if (c == u) atomicOr(err, 4);
+            if (i > b && cols[i - 1] >= c) atomicOr(err, 8);
+            // symmetric: u in N(c)
+            int64_t lo = off[c], hi = off[c + 1];
+            bool found = false;
+            while (lo < hi) {
+                int64_t mid = (lo + hi) >> 1;
+                int32_t x = cols[mid];
+                if (x == u) { found = true; break; }
+                if (x < u) lo = mid + 1; else hi = mid;
+            }
+            if (!found) atomicOr(err, 16);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- relabel kernels
+__global__ void k_degree_keys(const int64_t* __restrict__ off, int64_t n, uint64_t* keys, int* maxdeg) {
+    int local = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        int64_t d = off[v + 1] - off[v];
+        keys[v] = ((uint64_t)d << 32) | (uint64_t)v;
+        local = max(local, (int)d);
+    }
+    for (int o = 16; o; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(maxdeg, local);
+}
+
+__global__ void k_permutation(const uint64_t* __restrict__ sorted, int64_t n, int32_t* new2old, int32_t* old2new,
+                              int64_t* newdeg) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = sorted[p];
+        int32_t old = (int32_t)(k & 0xffffffffu);
+        new2old[p] = old;
+        old2new[old] = (int32_t)p;
+        newdeg[p] = (int64_t)(k >> 32);
+    }
+}
+
+// warp per new vertex p: emit (p, old2new[w]) keys for its old list
+__global__ void k_edge_keys(const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                            const int64_t* __restrict__ noff, const int32_t* __restrict__ new2old,
+                            const int32_t* __restrict__ old2new, int64_t n, uint64_t* ekeys) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = warp; p < n; p += nwarps) {
+        const int32_t old = new2old[p];
+        const int64_t b = off[old], e = off[old + 1], dst = noff[p];
+        for (int64_t i = b + lane; i < e; i += 32)
+            ekeys[dst + (i - b)] = ((uint64_t)p << 32) | (uint32_t)old2new[cols[i]];
+    }
+}
+
+__global__ void k_extract_cols(const uint64_t* __restrict__ ekeys, int64_t nnz, int32_t* cols) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+        cols[i] = (int32_t)(ekeys[i] & 0xffffffffu);
+}
+
+__global__ void k_up(const int64_t* __restrict__ off, const int32_t* __restrict__ cols, int64_t n, int32_t* up) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = off[v], hi = off[v + 1];
+        const int64_t b = lo;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (cols[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        up[v] = (int32_t)(lo - b);
+    }
+}
+
+__global__ void k_permute_labels(const uint32_t* __restrict__ labels, const int32_t* __restrict__ new2old, int64_t n,
+                                 uint32_t* out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        out[p] = labels[new2old[p]];
+}
+
+static int grid_for(int64_t items, int threads = 256) {
+    int64_t b = (items + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 64) b = 148 * 64;
+    return (int)b;
+}
+
+static int bits_for(uint64_t x) {
+    int b = 1;
+    while (b < 64 && (x >> b)) ++b;
+    return b;
+}
+
+static void free_graph(gsm_graph* h) {
+    if (!h) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(h->device);
+    DevGraph& g = h->g;
+    cudaStreamSynchronize(h->stream);
+    cudaFree(g.off);
+    cudaFree(g.cols);
+    cudaFree(g.up);
+    cudaFree(g.labels);
+    cudaFree(g.new2old);
+    cudaFree(g.old2new);
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    cudaSetDevice(cur);
+    delete h;
+}
+
+static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t* col_indices, const uint32_t* labels,
+                            int32_t on_device, const gsm_load_opts* opts, gsm_graph** out) {
+    if (!out) fail(GSM_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (opts && opts->struct_size != sizeof(gsm_load_opts)) fail(GSM_ERR_INVALID_ARGUMENT, "gsm_load_opts.struct_size mismatch");
+    if (n <= 0) fail(GSM_ERR_INVALID_GRAPH, "graph has no vertices");
+    if (n >= (int64_t)0x7fffffff) fail(GSM_ERR_INVALID_GRAPH, "more than 2^31-1 vertices");
+    if (!row_offsets || !col_indices) fail(GSM_ERR_INVALID_ARGUMENT, "CSR pointer is NULL");
+    int ndev = 0;
+    cudaError_t de = cudaGetDeviceCount(&ndev);
+    if (de != cudaSuccess || ndev == 0) {
+        (void)cudaGetLastError();
+        fail(GSM_ERR_NO_DEVICE, std::string("no CUDA device: ") + cudaGetErrorString(de));
+    }
+    const int device = opts ? opts->device : 0;
+    if (device < 0 || device >= ndev) fail(GSM_ERR_INVALID_ARGUMENT, "device ordinal out of range");
+    GSM_CUDA(cudaSetDevice(device));
+
+    std::unique_ptr<gsm_graph, void (*)(gsm_graph*)> h(new gsm_graph(), free_graph);
+    h->device = device;
+    if (opts && opts->stream) {
+        h->stream = (cudaStream_t)opts->stream;
+    } else {
+        GSM_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    cudaStream_t s = h->stream;
+    // keep freed pool memory cached between matches
+    cudaMemPool_t pool;
+    GSM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    GSM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+
+    int64_t nnz = 0;
+    if (on_device) GSM_CUDA(cudaMemcpyAsync(&nnz, row_offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    else nnz = row_offsets[n];
+    GSM_CUDA(cudaStreamSynchronize(s));
+    if (nnz < 0) fail(GSM_ERR_INVALID_GRAPH, "row_offsets[n] < 0");
+
+    // input replica on the device (borrowed zero-copy when already there)
+    DevBuf<int64_t> in_off;
+    DevBuf<int32_t> in_cols;
+    DevBuf<uint32_t> in_lab;
+    const int64_t* d_off = row_offsets;
+    const int32_t* d_cols = col_indices;
+    const uint32_t* d_lab = labels;
+    if (!on_device) {
+        in_off.ensure(n + 1, s);
+        in_cols.ensure(nnz, s);
+        GSM_CUDA(cudaMemcpyAsync(in_off.p, row_offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+        if (nnz) GSM_CUDA(cudaMemcpyAsync(in_cols.p, col_indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+        d_off = in_off.p;
+        d_cols = in_cols.p;
+        if (labels) {
+            in_lab.ensure(n, s);
+            GSM_CUDA(cudaMemcpyAsync(in_lab.p, labels, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
+            d_lab = in_lab.p;
+        }
+    }
+    if (opts && opts->validate) {
+        DevBuf<int> err;
+        err.ensure(1, s);
+        GSM_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), s));
+        k_validate_offsets<<<grid_for(n), 256, 0, s>>>(d_off, n, nnz, err.p);
+        GSM_LAUNCH("k_validate_offsets");
+        int herr = 0;
+        GSM_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        if (herr) fail(GSM_ERR_INVALID_GRAPH, "row_offsets are not a valid CSR offset array");
+        k_validate_lists<<<grid_for(n * 32), 256, 0, s>>>(d_off, d_cols, n, err.p);
+        GSM_LAUNCH("k_validate_lists");
+        GSM_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        if (herr & 2) fail(GSM_ERR_INVALID_GRAPH, "neighbour id out of range");
+        if (herr & 4) fail(GSM_ERR_INVALID_GRAPH, "self-loop");
+        if (herr & 8) fail(GSM_ERR_INVALID_GRAPH, "neighbour list not strictly ascending (unsorted or duplicate)");
+        if (herr & 16) fail(GSM_ERR_INVALID_GRAPH, "asymmetric edge (graph must be undirected)");
+    }
+
+    DevGraph& g = h->g;
+    g.n = n;
+    g.nnz = nnz;
+    GSM_CUDA(cudaMalloc(&g.off, sizeof(int64_t) * (n + 1)));
+    GSM_CUDA(cudaMalloc(&g.cols, sizeof(int32_t) * (nnz ? nnz : 1)));
+    GSM_CUDA(cudaMalloc(&g.up, sizeof(int32_t) * n));
+    GSM_CUDA(cudaMalloc(&g.new2old, sizeof(int32_t) * n));
+    GSM_CUDA(cudaMalloc(&g.old2new, sizeof(int32_t) * n));
+
+    // 1. rank by (degree, id)
+    {
+        DevBuf<uint64_t> keys, sorted;
+        DevBuf<int> maxdeg;
+        keys.ensure(n, s);
+        sorted.ensure(n, s);
+        maxdeg.ensure(1, s);
+        GSM_CUDA(cudaMemsetAsync(maxdeg.p, 0, sizeof(int), s));
+        k_degree_keys<<<grid_for(n), 256, 0, s>>>(d_off, n, keys.p, maxdeg.p);
+        GSM_LAUNCH("k_degree_keys");
+        int hmax = 0;
+        GSM_CUDA(cudaMemcpyAsync(&hmax, maxdeg.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        g.max_degree = hmax;
+        const int end_bit = 32 + bits_for((uint64_t)hmax);
+        size_t tmp_bytes = 0;
+        GSM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, sorted.p, n, 0, end_bit, s));
+        DevBuf<uint8_t> tmp;
+        tmp.ensure(tmp_bytes, s);
+        GSM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, n, 0, end_bit, s));
+        DevBuf<int64_t> newdeg;
+        newdeg.ensure(n, s);
+        k_permutation<<<grid_for(n), 256, 0, s>>>(sorted.p, n, g.new2old, g.old2new, newdeg.p);
+        GSM_LAUNCH("k_permutation");
+        GSM_CUDA(cudaMemsetAsync(g.off, 0, sizeof(int64_t), s));
+        size_t sb = 0;
+        GSM_CUDA(cub::DeviceScan::InclusiveSum(nullptr, sb, newdeg.p, g.off + 1, n, s));
+        DevBuf<uint8_t> stmp;
+        stmp.ensure(sb, s);
+        GSM_CUDA(cub::DeviceScan::InclusiveSum(stmp.p, sb, newdeg.p, g.off + 1, n, s));
+    }
+    // 2. relabelled, re-sorted lists
+    if (nnz > 0) {
+        DevBuf<uint64_t> ekeys, esorted;
+        ekeys.ensure(nnz, s);
+        esorted.ensure(nnz, s);
+        k_edge_keys<<<grid_for(n * 32), 256, 0, s>>>(d_off, d_cols, g.off, g.new2old, g.old2new, n, ekeys.p);
+        GSM_LAUNCH("k_edge_keys");
+        const int end_bit = 32 + bits_for((uint64_t)n);
+        size_t tmp_bytes = 0;
+        GSM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, ekeys.p, esorted.p, nnz, 0, end_bit, s));
+        DevBuf<uint8_t> tmp;
+        tmp.ensure(tmp_bytes, s);
+        GSM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, ekeys.p, esorted.p, nnz, 0, end_bit, s));
+        k_extract_cols<<<grid_for(nnz), 256, 0, s>>>(esorted.p, nnz, g.cols);
+        GSM_LAUNCH("k_extract_cols");
+    }
+    k_up<<<grid_for(n), 256, 0, s>>>(g.off, g.cols, n, g.up);
+    GSM_LAUNCH("k_up");
+    if (labels) {
+        GSM_CUDA(cudaMalloc(&g.labels, sizeof(uint32_t) * n));
+        k_permute_labels<<<grid_for(n), 256, 0, s>>>(d_lab, g.new2old, n, g.labels);
+        GSM_LAUNCH("k_permute_labels");
+        h->labeled = true;
+    }
+    GSM_CUDA(cudaStreamSynchronize(s));
+    *out = h.release();
+}
+
+}  // namespace gsm
+
+extern "C" {
+
+gsm_status gsm_load_graph(int64_t num_nodes, const int64_t* row_offsets, const int32_t* col_indices,
+                          const uint32_t* labels, int32_t pointers_on_device, const gsm_load_opts* opts,
+                          gsm_graph** out) {
+    try {
+        gsm::clear_error();
+        gsm::load_graph_impl(num_nodes, row_offsets, col_indices, labels, pointers_on_device, opts, out);
+        return GSM_OK;
+    } catch (const gsm::Failure& f) {
+        gsm::set_error(f.msg);
+        if (out) *out = nullptr;
+        return f.status;
+    } catch (const std::bad_alloc&) {
+        gsm::set_error("host allocation failed");
+        if (out) *out = nullptr;
+        return GSM_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        gsm::set_error("unexpected exception in gsm_load_graph");
+        if (out) *out = nullptr;
+        return GSM_ERR_CUDA;
+    }
+}
+
+gsm_status gsm_free(gsm_graph* g) {
+    gsm::free_graph(g);
+    return GSM_OK;
+}
+
+gsm_status gsm_graph_info(const gsm_graph* g, int64_t* num_nodes, int64_t* num_directed_edges, int32_t* labeled,
+                          int32_t* device) {
+    if (!g) {
+        gsm::set_error("graph is NULL");
+        return GSM_ERR_INVALID_ARGUMENT;
+    }
+    if (num_nodes) *num_nodes = g->g.n;
+    if (num_directed_edges) *num_directed_edges = g->g.nnz;
+    if (labeled) *labeled = g->labeled ? 1 : 0;
+    if (device) *device = g->device;
+    return GSM_OK;
+}
+
+const char* gsm_last_error(void) { return gsm::g_last_error.c_str(); }
+
+const char* gsm_version(void) { return "gsm-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"
+
+// accessors used by gsm_match.cu
+namespace gsm {
+const DevGraph& graph_of(const gsm_graph* h) { return h->g; }
+int device_of(const gsm_graph* h) { return h->device; }
+cudaStream_t stream_of(const gsm_graph* h) { return h->stream; }
+bool labeled_of(const gsm_graph* h) { return h->labeled; }
+}  // namespace gsm

@@ -1,0 +1,71 @@
+// gsm_internal.h — shared between the host plan, the driver and the kernels of
+// libgsm (product side).  Nothing here is visible across the C ABI.
+#pragma once
+
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "gsm.h"
+
+namespace gsm {
+
+constexpr int kMaxK = GSM_MAX_QUERY_NODES;
+
+// ----------------------------------------------------------------------------
+// Host plan (PreCompute_on_CPUs, Alg. 1 lines 1-5)
+// ----------------------------------------------------------------------------
+struct QueryPlan {
+    int k = 0;
+    uint32_t adj[kMaxK] = {};     // adjacency bitmask per query vertex
+    uint32_t qlabel[kMaxK] = {};  // labels (if use_labels)
+    bool use_labels = false;
+    int qdeg[kMaxK] = {};
+
+    // symmetry breaking: "constraints on node ID values", Grochow-Kellis
+    bool symmetric = false;
+    std::vector<std::pair<int, int>> conds;  // (a, b): f(a) ≺ f(b)
+    uint64_t aut_size = 1;
+    std::vector<std::vector<int8_t>> aut_list;  // all automorphisms (sigma[u]) if listed
+    bool aut_list_complete = false;
+
+    // order (Compute_query_node_sequence_info)
+    int order[kMaxK] = {};    // position -> query vertex
+    int pos[kMaxK] = {};      // query vertex -> position
+    int parent[kMaxK] = {};   // position -> earlier position (spanning tree)
+    uint32_t backward[kMaxK] = {};  // position -> mask of earlier adjacent positions (nn + ne)
+};
+
+// Validates and loads a gsm_query (connected; no loops/dups).
+// Returns GSM_OK or GSM_ERR_INVALID_QUERY / GSM_ERR_INVALID_ARGUMENT with msg.
+gsm_status load_query(const gsm_query* q, QueryPlan* plan, std::string* msg);
+
+// Aut(Q) order, GK conditions, optional automorphism list (<= list_cap).
+void compute_symmetry(QueryPlan* plan, bool with_conditions, size_t list_cap);
+
+// Greedy order: max d_M, min |C(u)|, max deg, min id (cand may be NULL).
+// forced_first >= 0 pins position 0 (root-subset sampling).
+void compute_order(QueryPlan* plan, const uint64_t* cand, int forced_first);
+
+// ----------------------------------------------------------------------------
+// Per-level device plan (Verify_Constraints at position i, Alg. 1 lines 10-14)
+// ----------------------------------------------------------------------------
+struct LevelPlan {
+    int32_t width;       // i: columns of an input row (positions 0..i-1)
+    int32_t qv;          // query vertex π[i]: cmask bit to test
+    int32_t check_mask;  // 0 when the cmask bit is implied (no labels, deg_Q <= |B(i)|)
+    int32_t nb;          // |B(i)|: earlier positions adjacent to π[i]
+    int32_t bpos[kMaxK];
+    int32_t nlo;         // positions j with f(π[j]) ≺ f(π[i])  (candidate must be larger)
+    int32_t lo[kMaxK];
+    int32_t nhi;         // positions j with f(π[i]) ≺ f(π[j])  (candidate must be smaller)
+    int32_t hi[kMaxK];
+    int32_t ninj;        // positions needing an explicit injectivity compare
+    int32_t inj[kMaxK];
+    int32_t count_only;  // last level in COUNT mode: count survivors, write nothing
+};
+
+LevelPlan make_level_plan(const QueryPlan& p, int i, bool count_only);
+
+}  // namespace gsm

@@ -1,0 +1,584 @@
+// gsm_kernels.cu — the sm_100a kernels of the GSM hot path.
+//
+// Integer work only: no tensor cores (nothing here is a dense contraction).
+// The roofline is memory: K1 streams the offsets/labels (HBM-bound); the
+// expand kernel is dominated by reads of candidate lists and dependent random
+// probes (cmask bytes, binary searches) into a CSR that is L2-resident for
+// small graphs and HBM-resident for large ones.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+
+#include "gsm_kernels.h"
+
+namespace gsm {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxGrid = 148 * 16;
+
+inline int grid_for(int64_t items, int threads = kThreads, int cap = kMaxGrid) {
+    int64_t b = (items + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, cap));
+}
+
+}  // namespace
+
+// ============================================================================
+// K1 candidate filter — Alg. 1 "Filter+Compute" (line 8), PAPER P:110, P:129,
+// compatible = same label and degree >= deg_Q(u).  Coalesced streaming
+// of offsets (8 B/vertex, each pair shared by neighbouring threads), labels
+// (4 B/vertex) and cmask writes (1-4 B/vertex).  |C(u)| via warp ballots:
+// lane u keeps popc(ballot(bit u)), one atomic per lane per warp at the end.
+// ============================================================================
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_filter(const int64_t* __restrict__ off,
+                                                     const uint32_t* __restrict__ labels, int64_t n,
+                                                     FilterQuery q, MaskT* __restrict__ cmask,
+                                                     unsigned long long* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long mine = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int64_t v = base + threadIdx.x;
+        uint32_t m = 0;
+        if (v < n) {
+            const int64_t d = off[v + 1] - off[v];
+            const uint32_t lab = labels ? labels[v] : 0u;
+#pragma unroll
+            for (int u = 0; u < kMaxK; ++u) {
+                if (u >= q.k) break;
+                const bool ok = (!q.use_labels || lab == q.qlabel[u]) && d >= q.qdeg[u];
+                m |= (uint32_t)ok << u;
+            }
+            cmask[v] = (MaskT)m;
+        }
+#pragma unroll
+        for (int u = 0; u < kMaxK; ++u) {
+            if (u >= q.k) break;
+            const unsigned b = __ballot_sync(0xffffffffu, (m >> u) & 1u);
+            if (lane == u) mine += __popc(b);
+        }
+    }
+    if (lane < q.k && mine) atomicAdd(&counts[lane], mine);
+}
+
+void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigned long long* counts,
+                   cudaStream_t s) {
+    const int grid = grid_for(g.n);
+    switch (mask_bytes_for(q.k)) {
+        case 1: k_filter<uint8_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint8_t*)cmask, counts); break;
+        case 2: k_filter<uint16_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint16_t*)cmask, counts); break;
+        default: k_filter<uint32_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint32_t*)cmask, counts); break;
+    }
+    GSM_LAUNCH("k_filter");
+}
+
+// ============================================================================
+// Roots: level-0 frontier = C(π[0]) (Alg. 1 line 11: "All-source BFS traversal
+// from c_set"), compacted in ascending (degree, id) rank; multi-GPU shards keep
+// every P-th root.  Stable two-pass block-scan compaction.
+// ============================================================================
+constexpr int kRootItems = 8;
+constexpr int64_t kRootTile = (int64_t)kThreads * kRootItems;
+
+template <typename MaskT>
+__device__ __forceinline__ int root_flags(const MaskT* cmask, int64_t n, int bit, int64_t tile, uint32_t* flags) {
+    const int64_t first = tile * kRootTile + (int64_t)threadIdx.x * kRootItems;
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < kRootItems; ++j) {
+        const int64_t v = first + j;
+        const uint32_t f = (v < n) ? ((cmask[v] >> bit) & 1u) : 0u;
+        flags[j] = f;
+        c += f;
+    }
+    return c;
+}
+
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_root_count(const MaskT* __restrict__ cmask, int64_t n, int bit,
+                                                         int64_t* __restrict__ tile_counts) {
+    using BlockReduce = cub::BlockReduce<int, kThreads>;
+    __shared__ typename BlockReduce::TempStorage tmp;
+    uint32_t flags[kRootItems];
+    const int c = root_flags(cmask, n, bit, blockIdx.x, flags);
+    const int total = BlockReduce(tmp).Sum(c);
+    if (threadIdx.x == 0) tile_counts[blockIdx.x] = total;
+}
+
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_root_write(const MaskT* __restrict__ cmask, int64_t n, int bit,
+                                                         const int64_t* __restrict__ tile_base, int shard,
+                                                         int nshards, int32_t* __restrict__ roots) {
+    using BlockScan = cub::BlockScan<int, kThreads>;
+    __shared__ typename BlockScan::TempStorage tmp;
+    uint32_t flags[kRootItems];
+    const int c = root_flags(cmask, n, bit, blockIdx.x, flags);
+    int excl;
+    BlockScan(tmp).ExclusiveSum(c, excl);
+    int64_t rank = tile_base[blockIdx.x] + excl;
+    const int64_t first = (int64_t)blockIdx.x * kRootTile + (int64_t)threadIdx.x * kRootItems;
+#pragma unroll
+    for (int j = 0; j < kRootItems; ++j) {
+        if (flags[j]) {
+            if (rank % nshards == shard) roots[rank / nshards] = (int32_t)(first + j);
+            ++rank;
+        }
+    }
+}
+
+int64_t launch_roots(const DevGraph& g, const void* cmask, int mask_bytes, int bit, int shard, int nshards,
+                     int32_t* roots, cudaStream_t s) {
+    const int64_t tiles = (g.n + kRootTile - 1) / kRootTile;
+    DevBuf<int64_t> counts, base;
+    counts.ensure(tiles, s);
+    base.ensure(tiles + 1, s);
+    switch (mask_bytes) {
+        case 1: k_root_count<uint8_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint8_t*)cmask, g.n, bit, counts.p); break;
+        case 2: k_root_count<uint16_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint16_t*)cmask, g.n, bit, counts.p); break;
+        default: k_root_count<uint32_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint32_t*)cmask, g.n, bit, counts.p); break;
+    }
+    GSM_LAUNCH("k_root_count");
+    GSM_CUDA(cudaMemsetAsync(base.p, 0, sizeof(int64_t), s));
+    size_t tb = 0;
+    GSM_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, counts.p, base.p + 1, tiles, s));
+    DevBuf<uint8_t> tmp;
+    tmp.ensure(tb, s);
+    GSM_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, counts.p, base.p + 1, tiles, s));
+    switch (mask_bytes) {
+        case 1: k_root_write<uint8_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint8_t*)cmask, g.n, bit, base.p, shard, nshards, roots); break;
+        case 2: k_root_write<uint16_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint16_t*)cmask, g.n, bit, base.p, shard, nshards, roots); break;
+        default: k_root_write<uint32_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint32_t*)cmask, g.n, bit, base.p, shard, nshards, roots); break;
+    }
+    GSM_LAUNCH("k_root_write");
+    int64_t total = 0;
+    GSM_CUDA(cudaMemcpyAsync(&total, base.p + tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    GSM_CUDA(cudaStreamSynchronize(s));
+    if (nshards <= 1) return total;
+    return total > shard ? (total - shard + nshards - 1) / nshards : 0;
+}
+
+template <typename MaskT>
+__global__ void k_root_subset(const MaskT* __restrict__ cmask, int bit, const int32_t* __restrict__ old2new, int64_t n,
+                              const int32_t* __restrict__ subset, int64_t len, int32_t* __restrict__ roots,
+                              unsigned long long* __restrict__ count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t o = subset[i];
+        if (o < 0 || o >= n) continue;
+        const int32_t v = old2new[o];
+        if ((cmask[v] >> bit) & 1u) roots[atomicAdd(count, 1ull)] = v;
+    }
+}
+
+int64_t launch_root_subset(const DevGraph& g, const void* cmask, int mask_bytes, int bit, const int32_t* subset_old,
+                           int64_t len, int32_t* roots, cudaStream_t s) {
+    DevBuf<unsigned long long> cnt;
+    cnt.ensure(1, s);
+    GSM_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
+    const int grid = grid_for(len);
+    switch (mask_bytes) {
+        case 1: k_root_subset<uint8_t><<<grid, kThreads, 0, s>>>((const uint8_t*)cmask, bit, g.old2new, g.n, subset_old, len, roots, cnt.p); break;
+        case 2: k_root_subset<uint16_t><<<grid, kThreads, 0, s>>>((const uint16_t*)cmask, bit, g.old2new, g.n, subset_old, len, roots, cnt.p); break;
+        default: k_root_subset<uint32_t><<<grid, kThreads, 0, s>>>((const uint32_t*)cmask, bit, g.old2new, g.n, subset_old, len, roots, cnt.p); break;
+    }
+    GSM_LAUNCH("k_root_subset");
+    unsigned long long h = 0;
+    GSM_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    GSM_CUDA(cudaStreamSynchronize(s));
+    return (int64_t)h;
+}
+
+// ============================================================================
+// Per-row plan (the "Advance" source).  The paper expands from the
+// spanning-tree parent; we pick, per partial result, the backward neighbour
+// whose admissible list segment is shortest (same result set, less work,
+// SURVEY §8(a) A4).  ID constraints restrict candidates to an open
+// interval (lo, hi) of new ids; because lists are sorted, the admissible part
+// of a list is a contiguous segment, located with up[a] (exact when the bound
+// is a itself) or a binary search.
+// ============================================================================
+__device__ __forceinline__ int64_t lower_bound_cols(const int32_t* __restrict__ cols, int64_t lo, int64_t hi,
+                                                    int64_t key) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)cols[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kThreads) k_plan_rows(const int32_t* __restrict__ F, int64_t R, LevelPlan L,
+                                                        const int64_t* __restrict__ off,
+                                                        const int32_t* __restrict__ cols,
+                                                        const int32_t* __restrict__ up, int64_t n,
+                                                        int64_t* __restrict__ rbeg, int64_t* __restrict__ rlen,
+                                                        uint8_t* __restrict__ rpiv) {
+    const int W = L.width;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t* row = F + r * W;
+        int64_t lov = -1, hiv = n;
+        for (int q = 0; q < L.nlo; ++q) lov = max(lov, (int64_t)row[L.lo[q]]);
+        for (int q = 0; q < L.nhi; ++q) hiv = min(hiv, (int64_t)row[L.hi[q]]);
+        int64_t bs = 0, bt = 0, blen = INT64_MAX;
+        int bq = 0;
+        int32_t ba = 0;
+        for (int q = 0; q < L.nb; ++q) {
+            const int32_t a = row[L.bpos[q]];
+            int64_t s0 = off[a], t0 = off[a + 1];
+            if (lov >= a || hiv <= a) {
+                const int64_t split = s0 + up[a];
+                if (lov >= a) s0 = split;
+                if (hiv <= a) t0 = split;
+            }
+            const int64_t len = t0 - s0;
+            if (len < blen) { blen = len; bs = s0; bt = t0; bq = q; ba = a; }
+        }
+        if (lov + 1 >= hiv || blen <= 0) {
+            bt = bs;
+        } else if (blen > 8) {
+            if (lov > ba) bs = lower_bound_cols(cols, bs, bt, lov + 1);
+            if (hiv < ba) bt = lower_bound_cols(cols, bs, bt, hiv);
+        }
+        rbeg[r] = bs;
+        rlen[r] = bt > bs ? bt - bs : 0;
+        rpiv[r] = (uint8_t)bq;
+    }
+}
+
+void launch_plan_rows(const DevGraph& g, const int32_t* F, int64_t R, const LevelPlan& L, int64_t* rbeg,
+                      int64_t* rlen, uint8_t* rpiv, cudaStream_t s) {
+    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, g.cols, g.up, g.n, rbeg, rlen, rpiv);
+    GSM_LAUNCH("k_plan_rows");
+}
+
+size_t scan_temp_bytes(int64_t R) {
+    size_t b = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, b, (const int64_t*)nullptr, (int64_t*)nullptr, R);
+    return b;
+}
+
+void launch_scan(const int64_t* rlen, int64_t R, int64_t* P, void* tmp, size_t tmp_bytes, cudaStream_t s) {
+    GSM_CUDA(cudaMemsetAsync(P, 0, sizeof(int64_t), s));
+    GSM_CUDA(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, rlen, P + 1, R, s));
+}
+
+// ============================================================================
+// Merge-path partition (the load-balancing role of Gunrock's LB advance, which
+// "maps the newly traversed edges to consecutive GPU threads"): the
+// merge of row ends A[r] = P[r+1] with work items 0..S-1 is cut into equal
+// diagonals, so every CTA gets TD (rows + items) regardless of degree skew.
+// ============================================================================
+__device__ __forceinline__ int64_t merge_path(const int64_t* __restrict__ A, int64_t R, int64_t S, int64_t d) {
+    int64_t lo = max((int64_t)0, d - S), hi = min(d, R);
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (A[mid] <= d - mid - 1) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_partition(const int64_t* __restrict__ P, int64_t R, int64_t S, int64_t D0, int64_t D1, int64_t TD,
+                            int64_t ntiles, int64_t* __restrict__ tile_ra) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = min(D0 + t * TD, D1);
+        tile_ra[t] = merge_path(P + 1, R, S, d);
+    }
+}
+
+void launch_partition(const int64_t* P, int64_t R, int64_t S, int64_t D0, int64_t D1, int64_t TD, int64_t ntiles,
+                      int64_t* tile_ra, cudaStream_t s) {
+    k_partition<<<grid_for(ntiles + 1), kThreads, 0, s>>>(P, R, S, D0, D1, TD, ntiles, tile_ra);
+    GSM_LAUNCH("k_partition");
+}
+
+// ============================================================================
+// Expand + verify + compact — Alg. 1 lines 11-13 fused in one kernel:
+//   Advance: each work item is one entry of a row's pivot segment;
+//   Compute: ID bounds, cmask bit of π[i], injectivity, and
+//            membership v in N(f(j)) for every other backward neighbour j
+//            (binary search in the sorted CSR list) — the tree and non-tree
+//            connection checks;
+//   Write_to_Partial: survivors are appended to a shared-memory
+//            staging tile (warp ballot + popc ranks, one shared atomic per
+//            warp), then ONE global atomicAdd per tile reserves the output
+//            range and the tile is copied out coalesced.  At the last level in
+//            COUNT mode nothing is written: survivors are only counted.
+// One CTA per merge-path tile (grid-stride); the tile's rows (entries, pivot
+// segment start, work offsets) are staged in shared memory first.
+// ============================================================================
+__device__ __forceinline__ bool in_list(const int64_t* __restrict__ off, const int32_t* __restrict__ cols, int32_t a,
+                                        int32_t v, unsigned& probes) {
+    int64_t lo = off[a], hi = off[a + 1];
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        const int32_t x = cols[mid];
+        ++probes;
+        if (x == v) return true;
+        if (x < v) lo = mid + 1; else hi = mid;
+    }
+    return false;
+}
+
+int64_t expand_tile(int width) {
+    if (width <= 4) return 512;
+    if (width <= 12) return 256;
+    return 128;
+}
+
+static size_t expand_smem(int64_t TD, int W, bool count_only) {
+    size_t b = sizeof(int64_t) * (TD + 1) * 2 + sizeof(int32_t) * (TD + 1) * W + (TD + 1);
+    b = (b + 15) & ~(size_t)15;
+    if (!count_only) b += sizeof(int32_t) * TD * (W + 1);
+    return b;
+}
+
+template <typename MaskT, bool kCountOnly>
+__global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int64_t TD = a.TD;
+    const int W = L.width;
+    int64_t* sP = reinterpret_cast<int64_t*>(smem);
+    int64_t* sBeg = sP + (TD + 1);
+    int32_t* sRow = reinterpret_cast<int32_t*>(sBeg + (TD + 1));
+    uint8_t* sPiv = reinterpret_cast<uint8_t*>(sRow + (TD + 1) * W);
+    size_t outoff = (sizeof(int64_t) * (TD + 1) * 2 + sizeof(int32_t) * (TD + 1) * W + (TD + 1) + 15) & ~(size_t)15;
+    int32_t* sOut = reinterpret_cast<int32_t*>(smem + outoff);
+    __shared__ int sCount;
+    __shared__ unsigned long long sBase;
+    __shared__ unsigned long long sRed[kWarps][5];  // survivors, items, mask, probes, lists
+
+    const int lane = threadIdx.x & 31;
+    const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
+    unsigned long long cnt = 0;
+    unsigned st_items = 0, st_mask = 0, st_probes = 0, st_lists = 0;
+
+    for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const int64_t d0 = a.D0 + t * TD;
+        const int64_t d1 = min(d0 + TD, a.D1);
+        const int64_t ra0 = a.tile_ra[t], ra1 = a.tile_ra[t + 1];
+        const int64_t ib0 = d0 - ra0, ib1 = d1 - ra1;
+        if (ib1 <= ib0) continue;  // block-uniform
+        const int64_t rlast = min(ra1, a.R - 1);
+        const int nrows = (int)(rlast - ra0 + 1);
+        __syncthreads();  // previous tile finished with shared memory
+        for (int lr = threadIdx.x; lr < nrows; lr += kThreads) {
+            sP[lr] = a.P[ra0 + lr];
+            sBeg[lr] = a.rbeg[ra0 + lr];
+            sPiv[lr] = a.rpiv[ra0 + lr];
+        }
+        {
+            const int32_t* src = a.F + ra0 * W;
+            const int nq = nrows * W;
+            for (int q = threadIdx.x; q < nq; q += kThreads) sRow[q] = src[q];
+        }
+        if (threadIdx.x == 0) sCount = 0;
+        __syncthreads();
+
+        for (int64_t base = ib0; base < ib1; base += kThreads) {
+            const int64_t x = base + threadIdx.x;
+            bool ok = false;
+            int lr = 0;
+            int32_t v = 0;
+            if (x < ib1) {
+                ++st_items;
+                int lo = 0, hi = nrows;  // largest lr with sP[lr] <= x
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (sP[mid] <= x) lo = mid + 1; else hi = mid;
+                }
+                lr = lo - 1;
+                v = a.cols[sBeg[lr] + (x - sP[lr])];
+                const int32_t* row = sRow + lr * W;
+                ok = true;
+                for (int q = 0; q < L.nlo && ok; ++q) ok = v > row[L.lo[q]];
+                for (int q = 0; q < L.nhi && ok; ++q) ok = v < row[L.hi[q]];
+                if (ok && L.check_mask) {
+                    ++st_mask;
+                    ok = (cmask[v] >> L.qv) & 1u;
+                }
+                for (int q = 0; q < L.ninj && ok; ++q) ok = v != row[L.inj[q]];
+                const int piv = sPiv[lr];
+                for (int q = 0; q < L.nb && ok; ++q)
+                    if (q != piv) {
+                        ++st_lists;
+                        ok = in_list(a.off, a.cols, row[L.bpos[q]], v, st_probes);
+                    }
+            }
+            if (kCountOnly) {
+                cnt += ok ? 1u : 0u;
+            } else {
+                const unsigned ball = __ballot_sync(0xffffffffu, ok);
+                int wbase = 0;
+                if (lane == 0 && ball) wbase = atomicAdd(&sCount, __popc(ball));
+                wbase = __shfl_sync(0xffffffffu, wbase, 0);
+                if (ok) {
+                    const int pos = wbase + __popc(ball & ((1u << lane) - 1u));
+                    int32_t* o = sOut + (int64_t)pos * (W + 1);
+                    const int32_t* row = sRow + lr * W;
+                    for (int c = 0; c < W; ++c) o[c] = row[c];
+                    o[W] = v;
+                }
+            }
+        }
+        if (!kCountOnly) {
+            __syncthreads();
+            const int total = sCount;
+            if (threadIdx.x == 0) sBase = total ? atomicAdd(a.out_count, (unsigned long long)total) : 0ull;
+            __syncthreads();
+            cnt += (threadIdx.x == 0) ? (unsigned long long)total : 0ull;
+            int32_t* dst = a.out + sBase * (W + 1);
+            const int nq = total * (W + 1);
+            for (int q = threadIdx.x; q < nq; q += kThreads) dst[q] = sOut[q];
+        }
+    }
+    // block reduction of the counters
+    unsigned long long v5[5] = {cnt, st_items, st_mask, st_probes, st_lists};
+#pragma unroll
+    for (int c = 0; c < 5; ++c)
+        for (int o = 16; o; o >>= 1) v5[c] += __shfl_xor_sync(0xffffffffu, v5[c], o);
+    __syncthreads();
+    if (lane == 0)
+        for (int c = 0; c < 5; ++c) sRed[threadIdx.x >> 5][c] = v5[c];
+    __syncthreads();
+    if (threadIdx.x < 5) {
+        unsigned long long s = 0;
+        for (int w = 0; w < kWarps; ++w) s += sRed[w][threadIdx.x];
+        if (s) {
+            if (threadIdx.x == 0) {
+                if (kCountOnly) atomicAdd(a.out_count, s);
+                atomicAdd(&a.stats[3], s);  // survivors
+            } else if (threadIdx.x < 4) {
+                atomicAdd(&a.stats[threadIdx.x - 1], s);  // items, mask_checked, probes
+            } else {
+                atomicAdd(&a.stats[4], s);  // membership lists searched
+            }
+        }
+    }
+}
+
+template <typename MaskT, bool kCountOnly>
+static void launch_expand_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
+    const size_t smem = expand_smem(a.TD, L.width, kCountOnly);
+    static bool configured = false;  // per template instance
+    if (!configured) {
+        GSM_CUDA(cudaFuncSetAttribute(k_expand<MaskT, kCountOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+        configured = true;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    GSM_CUDA(cudaGetDevice(&dev));
+    GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand<MaskT, kCountOnly>, kThreads, smem));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(a.ntiles, (int64_t)sms * std::max(per_sm, 1)));
+    k_expand<MaskT, kCountOnly><<<(unsigned)grid, kThreads, smem, s>>>(a, L);
+    GSM_LAUNCH("k_expand");
+}
+
+void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cudaStream_t s) {
+    const bool c = L.count_only != 0;
+    switch (mask_bytes) {
+        case 1: c ? launch_expand_t<uint8_t, true>(a, L, s) : launch_expand_t<uint8_t, false>(a, L, s); break;
+        case 2: c ? launch_expand_t<uint16_t, true>(a, L, s) : launch_expand_t<uint16_t, false>(a, L, s); break;
+        default: c ? launch_expand_t<uint32_t, true>(a, L, s) : launch_expand_t<uint32_t, false>(a, L, s); break;
+    }
+}
+
+// ============================================================================
+// Finalize (Alg. 1 line 16: "Return ... subgraph enumeration M").
+// ============================================================================
+__global__ void k_to_query_order(const int32_t* __restrict__ in, int64_t N, int k, const int32_t* __restrict__ order,
+                                 const int32_t* __restrict__ new2old, int32_t* __restrict__ out) {
+    const int64_t total = N * k;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / k;
+        const int j = (int)(i - r * k);
+        out[r * k + order[j]] = new2old[in[i]];
+    }
+}
+
+void launch_to_query_order(const int32_t* in, int64_t N, int k, const int32_t* order, const int32_t* new2old,
+                           int32_t* out, cudaStream_t s) {
+    k_to_query_order<<<grid_for(N * k), kThreads, 0, s>>>(in, N, k, order, new2old, out);
+    GSM_LAUNCH("k_to_query_order");
+}
+
+// all embeddings of an orbit: (f∘σ)(u) = f(σ(u))
+__global__ void k_aut_expand(const int32_t* __restrict__ in, int64_t N, int k, const int8_t* __restrict__ sig,
+                             int64_t num_aut, int32_t* __restrict__ out) {
+    const int64_t total = N * k * num_aut;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t rowid = i / k;
+        const int u = (int)(i - rowid * k);
+        const int64_t sidx = rowid / N;
+        const int64_t r = rowid - sidx * N;
+        out[i] = in[r * k + sig[sidx * k + u]];
+    }
+}
+
+void launch_aut_expand(const int32_t* in, int64_t N, int k, const int8_t* sigmas, int64_t num_aut, int32_t* out,
+                       cudaStream_t s) {
+    k_aut_expand<<<grid_for(N * k * num_aut), kThreads, 0, s>>>(in, N, k, sigmas, num_aut, out);
+    GSM_LAUNCH("k_aut_expand");
+}
+
+// Lexicographic sort: LSD over column groups packed into 64-bit keys
+// (b = bits per id; floor(64/b) columns per key), CUB radix sort passes.
+__global__ void k_iota(uint32_t* p, int64_t N) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
+__global__ void k_pack_keys(const int32_t* __restrict__ rows, const uint32_t* __restrict__ perm, int64_t N, int k,
+                            int c0, int c1, int b, uint64_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t* r = rows + (int64_t)perm[i] * k;
+        uint64_t key = 0;
+        for (int c = c0; c < c1; ++c) key = (key << b) | (uint32_t)r[c];
+        keys[i] = key;
+    }
+}
+
+__global__ void k_gather_rows(const int32_t* __restrict__ rows, const uint32_t* __restrict__ perm, int64_t N, int k,
+                              int32_t* __restrict__ out) {
+    const int64_t total = N * k;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / k;
+        out[i] = rows[(int64_t)perm[r] * k + (i - r * k)];
+    }
+}
+
+void sort_rows(const int32_t* rows, int64_t N, int k, int64_t n, int32_t* out, cudaStream_t s) {
+    if (N <= 0) return;
+    if (N > (int64_t)0xffffffffLL) fail(GSM_ERR_OUT_OF_MEMORY, "enumeration larger than 2^32 rows");
+    int b = 1;
+    while (b < 31 && ((uint64_t)(n - 1) >> b)) ++b;
+    const int per = std::max(1, 64 / b);
+    DevBuf<uint32_t> perm, perm2;
+    DevBuf<uint64_t> keys, keys2;
+    perm.ensure(N, s);
+    perm2.ensure(N, s);
+    keys.ensure(N, s);
+    keys2.ensure(N, s);
+    k_iota<<<grid_for(N), kThreads, 0, s>>>(perm.p, N);
+    GSM_LAUNCH("k_iota");
+    size_t tb = 0;
+    GSM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys2.p, perm.p, perm2.p, N, 0, 64, s));
+    DevBuf<uint8_t> tmp;
+    tmp.ensure(tb, s);
+    for (int c1 = k; c1 > 0; c1 -= per) {
+        const int c0 = std::max(0, c1 - per);
+        k_pack_keys<<<grid_for(N), kThreads, 0, s>>>(rows, perm.p, N, k, c0, c1, b, keys.p);
+        GSM_LAUNCH("k_pack_keys");
+        GSM_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys2.p, perm.p, perm2.p, N, 0, (c1 - c0) * b, s));
+        std::swap(perm.p, perm2.p);
+    }
+    k_gather_rows<<<grid_for(N * k), kThreads, 0, s>>>(rows, perm.p, N, k, out);
+    GSM_LAUNCH("k_gather_rows");
+}
+
+}  // namespace gsm

@@ -1,0 +1,77 @@
+// gsm_kernels.h — launchers for the hot-path kernels (gsm_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gsm_common.h"
+
+namespace gsm {
+
+struct FilterQuery {
+    int32_t k;
+    int32_t use_labels;
+    uint32_t qlabel[kMaxK];
+    int32_t qdeg[kMaxK];
+};
+
+// mask width: 1, 2 or 4 bytes per vertex (k <= 8, 16, 32)
+inline int mask_bytes_for(int k) { return k <= 8 ? 1 : (k <= 16 ? 2 : 4); }
+
+// K1 (Alg. 1 line 8): cmask[v] bit u = [label(v) = label_Q(u)] and [deg(v) >= deg_Q(u)];
+// counts[u] += |C(u)|  (counts must be zeroed by the caller).
+void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigned long long* counts,
+                   cudaStream_t s);
+
+// Roots: stable compaction of {v : bit `bit` of cmask[v]} in ascending new id, keeping global
+// rank r with r % nshards == shard (written at r / nshards).  Returns the number written.
+int64_t launch_roots(const DevGraph& g, const void* cmask, int mask_bytes, int bit, int shard, int nshards,
+                     int32_t* roots, cudaStream_t s);
+
+// Root subset (original ids, device array): new ids with the cmask bit set (order preserved).
+int64_t launch_root_subset(const DevGraph& g, const void* cmask, int mask_bytes, int bit, const int32_t* subset_old,
+                           int64_t len, int32_t* roots, cudaStream_t s);
+
+// Per-row pivot choice and candidate range (the "Advance" source list).
+void launch_plan_rows(const DevGraph& g, const int32_t* F, int64_t R, const LevelPlan& L, int64_t* rbeg,
+                      int64_t* rlen, uint8_t* rpiv, cudaStream_t s);
+
+// Inclusive scan of rlen into P[1..R] (P[0] = 0); returns nothing (caller reads P[R]).
+size_t scan_temp_bytes(int64_t R);
+void launch_scan(const int64_t* rlen, int64_t R, int64_t* P, void* tmp, size_t tmp_bytes, cudaStream_t s);
+
+// Merge-path partition of diagonals [D0, D1) into tiles of TD: tile_ra[t] for t = 0..ntiles.
+void launch_partition(const int64_t* P, int64_t R, int64_t S, int64_t D0, int64_t D1, int64_t TD, int64_t ntiles,
+                      int64_t* tile_ra, cudaStream_t s);
+
+struct ExpandArgs {
+    const int32_t* F;      // input rows (R x width)
+    int64_t R;
+    const int64_t* P;      // R+1 work offsets
+    const int64_t* rbeg;   // R pivot-range starts (index into cols)
+    const uint8_t* rpiv;   // R pivot index into L.bpos
+    const int64_t* tile_ra;
+    int64_t D0, D1, TD, ntiles;
+    const int64_t* off;
+    const int32_t* cols;
+    const void* cmask;
+    int32_t* out;          // survivors (width+1 ints each), unless count_only
+    unsigned long long* out_count;  // survivors (atomic)
+    unsigned long long* stats;      // [items, mask_checked, probes, survivors, lists]
+};
+
+// Tile size (merge steps per CTA) for a given input width.
+int64_t expand_tile(int width);
+
+// K2+K3+K4 fused: expand + verify + compact (Alg. 1 lines 11-13).
+void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cudaStream_t s);
+
+// Finalize ("Return ... subgraph enumeration M").
+void launch_to_query_order(const int32_t* in, int64_t N, int k, const int32_t* order, const int32_t* new2old,
+                           int32_t* out, cudaStream_t s);
+void launch_aut_expand(const int32_t* in, int64_t N, int k, const int8_t* sigmas, int64_t num_aut, int32_t* out,
+                       cudaStream_t s);
+// Lexicographic sort of N rows x k int32 columns (values in [0, n)).  Uses `out` as destination.
+void sort_rows(const int32_t* rows, int64_t N, int k, int64_t n, int32_t* out, cudaStream_t s);
+
+}  // namespace gsm

@@ -1,0 +1,546 @@
+// gsm_match.cu — gsm_match: the GSM driver (Alg. 1).
+//
+//   PreCompute_on_CPUs (lines 1-5)   -> gsm_plan.cpp (order, nn, ne, ID constraints)
+//   Filter_candidate_set (lines 6-9) -> K1 filter kernel + root compaction
+//   while |M[i]| < |Q| (lines 10-15) -> per position i: plan_rows, scan,
+//                                       merge-path partition, fused expand kernel
+//   return |M|/|Q| and M (line 16)   -> count reduction / finalize (id map,
+//                                       Aut-expansion, lexicographic sort)
+//
+// Chunked frontier ("memory linear to
+// matched subgraphs"): a position's work space (rows + candidate items, i.e.
+// its merge-path diagonals) is cut into chunks no larger than the next level's
+// row capacity.  Survivors <= candidate items, so a chunk can never overflow;
+// each chunk's output is consumed depth-first before the next chunk runs.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <vector>
+
+#include "gsm_common.h"
+#include "gsm_kernels.h"
+
+namespace gsm {
+
+const DevGraph& graph_of(const gsm_graph* h);
+int device_of(const gsm_graph* h);
+cudaStream_t stream_of(const gsm_graph* h);
+bool labeled_of(const gsm_graph* h);
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+inline double ms_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// Per-kernel CUDA-event bracketing (GSM_FLAG_PROFILE) + launch accounting.
+struct Recorder {
+    bool prof = false;
+    cudaStream_t s = 0;
+    gsm_result* res = nullptr;
+    struct Mark { int kind; cudaEvent_t a, b; };
+    std::vector<Mark> marks;
+    ~Recorder() {
+        for (auto& m : marks) {
+            cudaEventDestroy(m.a);
+            cudaEventDestroy(m.b);
+        }
+    }
+    template <class F>
+    void run(int kind, int launches, F&& f) {
+        res->kernel_launches += launches;
+        res->prof[kind].launches += launches;
+        if (!prof) { f(); return; }
+        Mark m{kind, nullptr, nullptr};
+        GSM_CUDA(cudaEventCreate(&m.a));
+        GSM_CUDA(cudaEventCreate(&m.b));
+        marks.push_back(m);
+        GSM_CUDA(cudaEventRecord(m.a, s));
+        f();
+        GSM_CUDA(cudaEventRecord(m.b, s));
+    }
+    void finish() {
+        if (!prof) return;
+        GSM_CUDA(cudaStreamSynchronize(s));
+        for (auto& m : marks) {
+            float ms = 0;
+            GSM_CUDA(cudaEventElapsedTime(&ms, m.a, m.b));
+            res->prof[m.kind].ms += ms;
+        }
+    }
+};
+
+struct LevelBufs {
+    DevBuf<int32_t> rows;  // frontier of this width (input rows of process(width))
+    int64_t cap_rows = 0;  // row capacity reserved for this frontier (0 = unbounded roots)
+    DevBuf<int64_t> rbeg, rlen, P, tile_ra;
+    DevBuf<uint8_t> rpiv, scan_tmp;
+    DevBuf<unsigned long long> out_count;
+    unsigned long long* stats = nullptr;  // 5 counters for this width's expand launches
+    double rows_in = 0;                   // rows staged by this width's expand launches
+};
+
+template <typename T>
+T read_scalar(const T* dptr, cudaStream_t s) {
+    T h{};
+    GSM_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    GSM_CUDA(cudaStreamSynchronize(s));
+    return h;
+}
+
+class Matcher {
+   public:
+    Matcher(const gsm_graph* gh, QueryPlan& plan, const gsm_match_opts& o, gsm_result* res, cudaStream_t s)
+        : g_(graph_of(gh)), plan_(plan), opts_(o), res_(res), s_(s) {
+        rec_.prof = (o.flags & GSM_FLAG_PROFILE) != 0;
+        rec_.s = s;
+        rec_.res = res;
+    }
+
+    void run();
+
+   private:
+    void process(int w, const int32_t* F, int64_t R);
+    void append_output(const int32_t* rows, int64_t R);
+    void finalize();
+
+    const DevGraph& g_;
+    QueryPlan& plan_;
+    const gsm_match_opts& opts_;
+    gsm_result* res_;
+    cudaStream_t s_;
+    Recorder rec_;
+
+    int k_ = 0;
+    int mask_bytes_ = 1;
+    bool count_mode_ = true;
+    DevBuf<uint8_t> cmask_;
+    std::vector<LevelPlan> lplan_;
+    std::vector<std::unique_ptr<LevelBufs>> lv_;  // index = width 1..k
+    DevBuf<unsigned long long> final_count_;      // COUNT mode: survivors at the last level
+    DevBuf<unsigned long long> stats_;            // 5 per width
+    DevBuf<int32_t> arena_;                       // ENUMERATE: rows in position order, new ids
+    int64_t arena_rows_ = 0;
+    int64_t budget_ = 0;
+    double t_expand_ms_ = 0;
+};
+
+void Matcher::run() {
+    const auto t_all = Clock::now();
+    k_ = plan_.k;
+    count_mode_ = opts_.mode == GSM_MODE_COUNT;
+    mask_bytes_ = mask_bytes_for(k_);
+
+    // ---- Filter_candidate_set (Alg. 1 lines 6-9): K1 over every data vertex
+    auto t0 = Clock::now();
+    FilterQuery fq;
+    std::memset(&fq, 0, sizeof(fq));
+    fq.k = k_;
+    fq.use_labels = plan_.use_labels ? 1 : 0;
+    for (int u = 0; u < k_; ++u) {
+        fq.qlabel[u] = plan_.qlabel[u];
+        fq.qdeg[u] = plan_.qdeg[u];
+    }
+    cmask_.ensure((size_t)g_.n * mask_bytes_, s_);
+    DevBuf<unsigned long long> counts;
+    counts.ensure(kMaxK, s_);
+    GSM_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * kMaxK, s_));
+    rec_.run(GSM_K_FILTER, 1, [&] { launch_filter(g_, fq, cmask_.p, counts.p, s_); });
+    res_->prof[GSM_K_FILTER].alg_bytes +=
+        (double)g_.n * (8.0 + (plan_.use_labels ? 4.0 : 0.0) + mask_bytes_);
+    unsigned long long hc[kMaxK];
+    GSM_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, s_));
+    GSM_CUDA(cudaStreamSynchronize(s_));
+    uint64_t cand[kMaxK];
+    bool empty = false;
+    for (int u = 0; u < k_; ++u) {
+        cand[u] = hc[u];
+        res_->candidates[u] = hc[u];
+        if (hc[u] == 0) empty = true;
+    }
+    // ---- query order with the exact |C(u)|
+    compute_order(&plan_, cand, opts_.root_subset ? 0 : -1);
+    for (int i = 0; i < k_; ++i) res_->order[i] = plan_.order[i];
+    res_->num_levels = k_;
+    res_->width = k_;
+    lv_.resize(k_ + 1);
+    for (int w = 0; w <= k_; ++w) lv_[w].reset(new LevelBufs());
+    lplan_.resize(k_);
+    for (int i = 1; i < k_; ++i) lplan_[i] = make_level_plan(plan_, i, count_mode_ && i == k_ - 1);
+
+    // ---- roots = C(π[0]) (level-0 frontier)
+    int64_t R0 = 0;
+    if (!empty && (int64_t)k_ <= g_.n) {
+        const int bit = plan_.order[0];
+        if (opts_.root_subset) {
+            DevBuf<int32_t> sub;
+            sub.ensure(opts_.root_subset_len, s_);
+            GSM_CUDA(cudaMemcpyAsync(sub.p, opts_.root_subset, sizeof(int32_t) * opts_.root_subset_len,
+                                     cudaMemcpyHostToDevice, s_));
+            lv_[1]->rows.ensure(opts_.root_subset_len, s_);
+            rec_.run(GSM_K_ROOTS, 1, [&] {
+                R0 = launch_root_subset(g_, cmask_.p, mask_bytes_, bit, sub.p, opts_.root_subset_len,
+                                        lv_[1]->rows.p, s_);
+            });
+        } else {
+            const int nsh = opts_.num_shards > 1 ? opts_.num_shards : 1;
+            const int sh = nsh > 1 ? opts_.shard_index : 0;
+            lv_[1]->rows.ensure(g_.n, s_);
+            rec_.run(GSM_K_ROOTS, 3, [&] {
+                R0 = launch_roots(g_, cmask_.p, mask_bytes_, bit, sh, nsh, lv_[1]->rows.p, s_);
+            });
+        }
+        res_->prof[GSM_K_ROOTS].alg_bytes += 2.0 * (double)g_.n * mask_bytes_ + 4.0 * (double)R0;
+    }
+    res_->level_rows[0] = (uint64_t)R0;
+    res_->ms_filter = (float)ms_since(t0);
+
+    // ---- verify iterations (Alg. 1 lines 10-15)
+    t0 = Clock::now();
+    final_count_.ensure(1, s_);
+    GSM_CUDA(cudaMemsetAsync(final_count_.p, 0, sizeof(unsigned long long), s_));
+    stats_.ensure(5 * (kMaxK + 1), s_);
+    GSM_CUDA(cudaMemsetAsync(stats_.p, 0, sizeof(unsigned long long) * 5 * (kMaxK + 1), s_));
+    for (int w = 1; w < k_; ++w) lv_[w]->stats = stats_.p + 5 * w;
+
+    size_t free_b = 0, total_b = 0;
+    GSM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    budget_ = opts_.mem_budget_bytes ? (int64_t)opts_.mem_budget_bytes : (int64_t)(free_b / 4);
+    // per-width share of the budget for frontiers of width 2..k (k only when enumerating)
+    const int nfront = count_mode_ ? std::max(0, k_ - 2) : k_ - 1;
+    for (int w = 2; w <= k_; ++w) {
+        const int64_t share = nfront > 0 ? budget_ / nfront : budget_;
+        const int64_t per_row = 4 * w + 8 * 3 + 1 + 1;  // rows + rbeg/rlen/P + piv + tile slack
+        lv_[w]->cap_rows = std::max<int64_t>(share / per_row, 1);
+    }
+
+    uint64_t found = 0;
+    if (k_ == 1) {
+        found = (uint64_t)R0;
+        if (!count_mode_ && R0 > 0) append_output(lv_[1]->rows.p, R0);
+    } else if (R0 > 0) {
+        process(1, lv_[1]->rows.p, R0);
+        if (count_mode_) found = read_scalar(final_count_.p, s_);
+        else found = (uint64_t)arena_rows_;
+    }
+    // per-level stats -> result + algorithmic bytes of the expand kernel
+    if (k_ > 1) {
+        std::vector<unsigned long long> hs(5 * (kMaxK + 1));
+        GSM_CUDA(cudaMemcpyAsync(hs.data(), stats_.p, sizeof(unsigned long long) * hs.size(),
+                                 cudaMemcpyDeviceToHost, s_));
+        GSM_CUDA(cudaStreamSynchronize(s_));
+        double eb = 0;
+        for (int w = 1; w < k_; ++w) {
+            const unsigned long long* st = hs.data() + 5 * w;
+            const LevelPlan& L = lplan_[w];
+            // staged rows (entries + work offset + pivot start + pivot index), list entries read,
+            // cmask bytes, membership lists (offset pair) and probes, survivor rows written
+            eb += lv_[w]->rows_in * (4.0 * w + 8 + 8 + 1) + 4.0 * st[0] + (double)mask_bytes_ * st[1] +
+                  16.0 * st[4] + 4.0 * st[2] + (L.count_only ? 0.0 : 4.0 * (w + 1) * st[3]);
+            res_->level_work[w] = st[0];
+            res_->level_rows[w] = st[3];  // partial results with w+1 matched positions
+        }
+        res_->prof[GSM_K_EXPAND].alg_bytes += eb;
+    }
+    res_->count_unique = found;
+    const bool expand_orbits = plan_.symmetric && !(opts_.flags & GSM_FLAG_UNIQUE);
+    res_->count = expand_orbits ? found * plan_.aut_size : found;
+    res_->symmetric = plan_.symmetric ? 1 : 0;
+    res_->ms_expand = (float)ms_since(t0);
+
+    t0 = Clock::now();
+    if (!count_mode_) finalize();
+    res_->ms_finalize = (float)ms_since(t0);
+    rec_.finish();
+    res_->ms_total = (float)ms_since(t_all);
+}
+
+void Matcher::process(int w, const int32_t* F, int64_t R) {
+    if (R <= 0) return;
+    LevelBufs& B = *lv_[w];
+    const LevelPlan& L = lplan_[w];
+    // per-row pivot choice and admissible segment
+    B.rbeg.ensure(R, s_);
+    B.rlen.ensure(R, s_);
+    B.rpiv.ensure(R, s_);
+    B.P.ensure(R + 1, s_);
+    const size_t tb = scan_temp_bytes(R);
+    B.scan_tmp.ensure(tb, s_);
+    rec_.run(GSM_K_PLAN, 1, [&] { launch_plan_rows(g_, F, R, L, B.rbeg.p, B.rlen.p, B.rpiv.p, s_); });
+    res_->prof[GSM_K_PLAN].alg_bytes += (double)R * (4.0 * w + 16.0 * L.nb + 8 + 8 + 1);
+    rec_.run(GSM_K_SCAN, 1, [&] { launch_scan(B.rlen.p, R, B.P.p, B.scan_tmp.p, tb, s_); });
+    res_->prof[GSM_K_SCAN].alg_bytes += (double)R * 16.0;
+    const int64_t S = read_scalar(B.P.p + R, s_);
+    if (S <= 0) return;
+
+    const int64_t total = R + S;
+    const int64_t TD = expand_tile(w);
+    const bool last = (w == k_ - 1);
+    int64_t chunk;
+    if (last && count_mode_) {
+        chunk = TD * ((int64_t)1 << 22);  // only bounds the tile array
+    } else {
+        chunk = std::min<int64_t>(total, lv_[w + 1]->cap_rows);
+        if (chunk < TD) chunk = std::min<int64_t>(total, TD);
+        lv_[w + 1]->rows.ensure((size_t)chunk * (w + 1), s_);
+        lv_[w + 1]->out_count.ensure(1, s_);
+    }
+    chunk = std::min(chunk, total);
+    B.tile_ra.ensure((size_t)((chunk + TD - 1) / TD + 1), s_);
+
+    ExpandArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.F = F;
+    a.R = R;
+    a.P = B.P.p;
+    a.rbeg = B.rbeg.p;
+    a.rpiv = B.rpiv.p;
+    a.tile_ra = B.tile_ra.p;
+    a.TD = TD;
+    a.off = g_.off;
+    a.cols = g_.cols;
+    a.cmask = cmask_.p;
+    a.stats = B.stats;
+    B.rows_in += (double)R;
+    for (int64_t D0 = 0; D0 < total; D0 += chunk) {
+        const int64_t D1 = std::min(D0 + chunk, total);
+        const int64_t ntiles = (D1 - D0 + TD - 1) / TD;
+        rec_.run(GSM_K_SCAN, 1, [&] { launch_partition(B.P.p, R, S, D0, D1, TD, ntiles, B.tile_ra.p, s_); });
+        res_->prof[GSM_K_SCAN].alg_bytes += (double)(ntiles + 1) * 8.0 * 2;
+        a.D0 = D0;
+        a.D1 = D1;
+        a.ntiles = ntiles;
+        res_->num_chunks++;
+        if (last && count_mode_) {
+            a.out = nullptr;
+            a.out_count = final_count_.p;
+            rec_.run(GSM_K_EXPAND, 1, [&] { launch_expand(a, L, mask_bytes_, s_); });
+            continue;
+        }
+        LevelBufs& N = *lv_[w + 1];
+        GSM_CUDA(cudaMemsetAsync(N.out_count.p, 0, sizeof(unsigned long long), s_));
+        a.out = N.rows.p;
+        a.out_count = N.out_count.p;
+        rec_.run(GSM_K_EXPAND, 1, [&] { launch_expand(a, L, mask_bytes_, s_); });
+        const int64_t R2 = (int64_t)read_scalar(N.out_count.p, s_);
+        if (R2 == 0) continue;
+        if (last) append_output(N.rows.p, R2);
+        else process(w + 1, N.rows.p, R2);
+    }
+}
+
+void Matcher::append_output(const int32_t* rows, int64_t R) {
+    const int64_t need = arena_rows_ + R;
+    if ((size_t)(need * k_) > arena_.n) {
+        size_t cap = std::max<size_t>((size_t)need * k_, arena_.n + arena_.n / 2);
+        int32_t* np = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * cap, s_));
+        if (arena_rows_) GSM_CUDA(cudaMemcpyAsync(np, arena_.p, sizeof(int32_t) * arena_rows_ * k_,
+                                                  cudaMemcpyDeviceToDevice, s_));
+        arena_.release();
+        arena_.p = np;
+        arena_.n = cap;
+        arena_.s = s_;
+    }
+    GSM_CUDA(cudaMemcpyAsync(arena_.p + arena_rows_ * k_, rows, sizeof(int32_t) * R * k_,
+                             cudaMemcpyDeviceToDevice, s_));
+    arena_rows_ = need;
+}
+
+void Matcher::finalize() {
+    const int64_t N = arena_rows_;
+    const bool expand = plan_.symmetric && !(opts_.flags & GSM_FLAG_UNIQUE);
+    const int64_t naut = expand ? (int64_t)plan_.aut_list.size() : 1;
+    const int64_t total = N * naut;
+    res_->num_rows = (uint64_t)total;
+    if (total == 0) return;
+    // 1. position order -> query-vertex order, new ids -> original ids
+    DevBuf<int32_t> dorder, q;
+    dorder.ensure(k_, s_);
+    GSM_CUDA(cudaMemcpyAsync(dorder.p, plan_.order, sizeof(int32_t) * k_, cudaMemcpyHostToDevice, s_));
+    q.ensure((size_t)N * k_, s_);
+    rec_.run(GSM_K_FINALIZE, 1, [&] { launch_to_query_order(arena_.p, N, k_, dorder.p, g_.new2old, q.p, s_); });
+    arena_.release();
+    // 2. all embeddings = {f∘σ : σ in Aut(Q)} of every representative
+    DevBuf<int32_t> all;
+    const int32_t* src = q.p;
+    if (expand && naut > 1) {
+        std::vector<int8_t> sig((size_t)naut * k_);
+        for (int64_t a = 0; a < naut; ++a)
+            for (int u = 0; u < k_; ++u) sig[a * k_ + u] = plan_.aut_list[a][u];
+        DevBuf<int8_t> dsig;
+        dsig.ensure(sig.size(), s_);
+        GSM_CUDA(cudaMemcpyAsync(dsig.p, sig.data(), sig.size(), cudaMemcpyHostToDevice, s_));
+        all.ensure((size_t)total * k_, s_);
+        rec_.run(GSM_K_FINALIZE, 1, [&] { launch_aut_expand(q.p, N, k_, dsig.p, naut, all.p, s_); });
+        GSM_CUDA(cudaStreamSynchronize(s_));
+        src = all.p;
+    }
+    // 3. lexicographic sort into the library-owned result buffer
+    int32_t* out = nullptr;
+    GSM_CUDA(cudaMalloc(&out, sizeof(int32_t) * (size_t)total * k_));
+    try {
+        rec_.run(GSM_K_FINALIZE, 4, [&] { sort_rows(src, total, k_, g_.n, out, s_); });
+        GSM_CUDA(cudaStreamSynchronize(s_));
+    } catch (...) {
+        cudaFree(out);
+        throw;
+    }
+    res_->rows = out;
+}
+
+void match_impl(const gsm_graph* gh, const gsm_query* q, const gsm_match_opts* user_opts, gsm_result* out) {
+    if (!gh) fail(GSM_ERR_INVALID_ARGUMENT, "graph is NULL");
+    gsm_match_opts opts;
+    std::memset(&opts, 0, sizeof(opts));
+    if (user_opts) {
+        if (user_opts->struct_size != sizeof(gsm_match_opts)) fail(GSM_ERR_INVALID_ARGUMENT, "gsm_match_opts.struct_size mismatch");
+        opts = *user_opts;
+    } else {
+        opts.struct_size = sizeof(opts);
+        opts.mode = GSM_MODE_COUNT;
+    }
+    if (opts.mode != GSM_MODE_COUNT && opts.mode != GSM_MODE_ENUMERATE) fail(GSM_ERR_INVALID_ARGUMENT, "bad mode");
+    if (opts.num_shards > 1 && (opts.shard_index < 0 || opts.shard_index >= opts.num_shards))
+        fail(GSM_ERR_INVALID_ARGUMENT, "shard_index out of range");
+    if (opts.root_subset_len < 0 || (opts.root_subset_len > 0 && !opts.root_subset))
+        fail(GSM_ERR_INVALID_ARGUMENT, "bad root_subset");
+    if (!opts.root_subset) opts.root_subset_len = 0;
+
+    const auto t0 = Clock::now();
+    QueryPlan plan;
+    std::string msg;
+    gsm_status st = load_query(q, &plan, &msg);
+    if (st != GSM_OK) fail(st, msg);
+    if (plan.use_labels && !labeled_of(gh)) fail(GSM_ERR_INVALID_ARGUMENT, "query has labels but the data graph is unlabeled");
+
+    const bool want_sym = !(opts.flags & GSM_FLAG_NO_SYMMETRY) && !opts.root_subset;
+    const bool need_list = opts.mode == GSM_MODE_ENUMERATE && !(opts.flags & GSM_FLAG_UNIQUE);
+    compute_symmetry(&plan, want_sym, need_list ? (size_t)1 << 16 : 0);
+    if (need_list && plan.symmetric && !plan.aut_list_complete) compute_symmetry(&plan, false, 0);
+    if ((opts.flags & GSM_FLAG_UNIQUE) && !plan.symmetric && plan.aut_size > 1)
+        fail(GSM_ERR_INVALID_ARGUMENT, "GSM_FLAG_UNIQUE cannot be combined with NO_SYMMETRY or root_subset");
+    out->automorphisms = plan.aut_size;
+
+    const int dev = device_of(gh);
+    int prev = 0;
+    GSM_CUDA(cudaGetDevice(&prev));
+    GSM_CUDA(cudaSetDevice(dev));
+    out->device = dev;
+    cudaStream_t s = opts.stream ? (cudaStream_t)opts.stream : stream_of(gh);
+    const float plan_ms = (float)ms_since(t0);
+    try {
+        Matcher m(gh, plan, opts, out, s);
+        m.run();
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        cudaSetDevice(prev);
+        throw;
+    }
+    out->ms_plan = plan_ms;
+    out->ms_total += plan_ms;
+    cudaSetDevice(prev);
+}
+
+}  // namespace
+}  // namespace gsm
+
+extern "C" {
+
+gsm_status gsm_match(const gsm_graph* g, const gsm_query* q, const gsm_match_opts* opts, gsm_result* out) {
+    if (!out) {
+        gsm::set_error("out is NULL");
+        return GSM_ERR_INVALID_ARGUMENT;
+    }
+    std::memset(out, 0, sizeof(*out));
+    try {
+        gsm::clear_error();
+        gsm::match_impl(g, q, opts, out);
+        return GSM_OK;
+    } catch (const gsm::Failure& f) {
+        if (out->rows) cudaFree(out->rows);
+        std::memset(out, 0, sizeof(*out));
+        gsm::set_error(f.msg);
+        return f.status;
+    } catch (const std::bad_alloc&) {
+        std::memset(out, 0, sizeof(*out));
+        gsm::set_error("host allocation failed");
+        return GSM_ERR_OUT_OF_MEMORY;
+    } catch (...) {
+        std::memset(out, 0, sizeof(*out));
+        gsm::set_error("unexpected exception in gsm_match");
+        return GSM_ERR_CUDA;
+    }
+}
+
+gsm_status gsm_result_free(gsm_result* r) {
+    if (!r) return GSM_OK;
+    if (r->rows) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(r->device);
+        cudaFree(r->rows);
+        cudaSetDevice(prev);
+    }
+    r->rows = nullptr;
+    r->num_rows = 0;
+    return GSM_OK;
+}
+
+gsm_status gsm_result_copy_rows(const gsm_result* r, int32_t* dst, int32_t dst_on_device) {
+    if (!r || (!dst && r->num_rows)) {
+        gsm::set_error("bad arguments to gsm_result_copy_rows");
+        return GSM_ERR_INVALID_ARGUMENT;
+    }
+    if (!r->num_rows) return GSM_OK;
+    if (!r->rows) {
+        gsm::set_error("result has no rows (COUNT mode or already freed)");
+        return GSM_ERR_INVALID_ARGUMENT;
+    }
+    cudaError_t e = cudaMemcpy(dst, r->rows, sizeof(int32_t) * r->num_rows * (size_t)r->width,
+                               dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+        gsm::set_error(std::string("cudaMemcpy: ") + cudaGetErrorString(e));
+        return GSM_ERR_CUDA;
+    }
+    return GSM_OK;
+}
+
+gsm_status gsm_plan_query(const gsm_query* q, const uint64_t* cand, uint32_t flags, gsm_plan_info* out) {
+    if (!out) {
+        gsm::set_error("out is NULL");
+        return GSM_ERR_INVALID_ARGUMENT;
+    }
+    std::memset(out, 0, sizeof(*out));
+    try {
+        gsm::clear_error();
+        gsm::QueryPlan plan;
+        std::string msg;
+        gsm_status st = gsm::load_query(q, &plan, &msg);
+        if (st != GSM_OK) {
+            gsm::set_error(msg);
+            return st;
+        }
+        gsm::compute_symmetry(&plan, !(flags & GSM_FLAG_NO_SYMMETRY), 0);
+        gsm::compute_order(&plan, cand, -1);
+        out->k = plan.k;
+        for (int i = 0; i < plan.k; ++i) {
+            out->order[i] = plan.order[i];
+            out->parent[i] = plan.parent[i];
+            out->backward[i] = plan.backward[i];
+        }
+        out->num_conditions = (int32_t)plan.conds.size();
+        for (size_t c = 0; c < plan.conds.size(); ++c) {
+            out->cond_lo[c] = plan.conds[c].first;
+            out->cond_hi[c] = plan.conds[c].second;
+        }
+        out->automorphisms = plan.aut_size;
+        return GSM_OK;
+    } catch (...) {
+        gsm::set_error("unexpected exception in gsm_plan_query");
+        return GSM_ERR_INVALID_QUERY;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,320 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element on the same seeded inputs.  Integer work => bit-exact: equal counts
+and identical sorted row lists.  Unique mode has several valid
+representative sets, so it is compared after canonicalisation f -> min_σ f∘σ
+(SURVEY §8(c) amb. 9/13) plus a check that the GPU rows are valid embeddings."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gsm_inputs as gi
+import oracle
+from oracle import closed_forms as cf
+from paper_2003_01527_b200 import gsm
+
+from gpu_helpers import assert_rows_equal, is_sorted_unique, load, run
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def check_all_modes(g, q, G=None, what="", budget=0):
+    own = G is None
+    if own:
+        G = load(g)
+    try:
+        cnt, ref = oracle.match(g, q)
+        aut = oracle.automorphisms(q)
+        kw = {"mem_budget_bytes": budget} if budget else {}
+        # all embeddings (symmetric search + Aut expansion)
+        c, rows, r = run(G, q, "enumerate", **kw)
+        assert c == cnt, (what, "all", c, cnt)
+        assert_rows_equal(rows, ref, what + " all")
+        c2, _, _ = run(G, q, "count", **kw)
+        assert c2 == cnt, (what, "count", c2, cnt)
+        # direct search, no ID constraints
+        c3, rows3, _ = run(G, q, "enumerate", flags=gsm.GSM_FLAG_NO_SYMMETRY, **kw)
+        assert c3 == cnt
+        assert_rows_equal(rows3, ref, what + " nosym")
+        # one per orbit
+        cu, rowsu, ru = run(G, q, "enumerate", flags=gsm.GSM_FLAG_UNIQUE, **kw)
+        uniq = oracle.unique(ref, aut)
+        assert cu == len(uniq) and ru.automorphisms == len(aut), (what, cu, len(uniq))
+        assert is_sorted_unique(rowsu)
+        if len(rowsu):
+            # canonical forms of the GPU representatives = the oracle's orbit set; with
+            # cu == len(uniq) this also proves one representative per orbit, and each
+            # representative is f∘σ of a valid embedding, hence valid itself
+            assert_rows_equal(oracle.unique(rowsu, aut), uniq, what + " unique(canonical)")
+        cuc, _, _ = run(G, q, "count", flags=gsm.GSM_FLAG_UNIQUE, **kw)
+        assert cuc == len(uniq)
+    finally:
+        if own:
+            G.free()
+
+
+def test_spec_golden_on_gpu():
+    ex = json.load(open(os.path.join(HERE, "golden", "spec_examples.json")))["examples"]
+    for e in ex:
+        d, qd = e["data"], e["query"]
+        g = gi.from_edge_list(d["num_nodes"], d["edges"])
+        if "labels" in d:
+            g = g.with_labels(np.asarray(d["labels"], np.uint32))
+        q = gi.Query(qd["num_nodes"], [tuple(x) for x in qd["edges"]], qd.get("labels"))
+        G = load(g)
+        try:
+            c, rows, r = run(G, q, "enumerate")
+            assert c == e["all"], e["cite"]
+            cu, rowsu, _ = run(G, q, "enumerate", flags=gsm.GSM_FLAG_UNIQUE)
+            assert cu == e["unique"], e["cite"]
+            if "unique_node_sets" in e:
+                assert sorted(sorted(x) for x in rowsu.tolist()) == e["unique_node_sets"]
+        finally:
+            G.free()
+
+
+def test_random_instances_match_oracle():
+    """SPEC acceptance criterion 2: >= 200 instances, G(30,0.2) and
+    G(50,0.1), unlabeled and 3 labels, connected 3-5-node queries."""
+    n_inst = 0
+    for seed in range(1, 26):
+        for (n, pn, pd) in [(30, 1, 5), (50, 1, 10)]:
+            g0 = gi.random_gnp(n, pn, pd, seed)
+            for nl in (0, 3):
+                g = g0.with_labels(gi.uniform_labels(n, 3, seed)) if nl else g0
+                G = load(g)
+                try:
+                    for j in range(2):
+                        k = 3 + (seed + j) % 3
+                        q = gi.random_connected_query(k, (seed + j) % 3, seed * 101 + j * 7 + n, nl)
+                        check_all_modes(g, q, G, what=f"seed{seed} n{n} nl{nl} {q.name}")
+                        n_inst += 1
+                finally:
+                    G.free()
+    assert n_inst >= 200
+
+
+@pytest.mark.parametrize("qname", ["K2", "K3", "P3", "P4", "S3", "C4", "K4", "C5", "house", "diamond", "tailed_triangle"])
+def test_named_queries_on_random_graphs(qname):
+    for seed in (1, 2):
+        g = gi.random_gnp(60, 1, 6, seed)
+        check_all_modes(g, gi.query(qname), what=f"{qname} s{seed}")
+    g = gi.rmat(10, 8, seed=4)
+    check_all_modes(g, gi.query(qname), what=f"{qname} rmat10")
+
+
+def test_labeled_named_queries():
+    g = gi.rmat(11, 8, seed=5).with_labels(gi.uniform_labels(2048, 3, 5))
+    G = load(g)
+    try:
+        for qname, ql in [("P4", [0, 1, 2, 0]), ("P4", [1, 2, 2, 1]), ("S3", [0, 1, 1, 2]), ("S3", [0, 1, 2, 2]),
+                          ("house", [0, 1, 2, 0, 1]), ("house", [0, 0, 1, 1, 2]), ("K3", [0, 0, 1]),
+                          ("C4", [0, 1, 0, 1]), ("K4", [0, 0, 0, 0])]:
+            check_all_modes(g, gi.query(qname, ql), G, what=f"{qname}{ql}")
+    finally:
+        G.free()
+
+
+def test_closed_forms_on_gpu():
+    for n in (5, 8):
+        G = load(gi.complete(n))
+        try:
+            for qname in ["K3", "P4", "C4", "K4", "house"]:
+                q = gi.query(qname)
+                assert run(G, q)[0] == cf.complete_graph(n, q.num_nodes)
+        finally:
+            G.free()
+    G = load(gi.petersen())
+    try:
+        assert run(G, gi.query("C5"))[0] == 120
+        assert run(G, gi.query("K3"))[0] == 0
+    finally:
+        G.free()
+    gg = gi.grid(80, 60, seed=3)
+    G = load(gg)
+    try:
+        assert run(G, gi.query("K4"))[0] == cf.grid_diag_k4(gg.meta["d2"])
+        assert run(G, gi.query("K3"))[0] == cf.grid_diag_k3(gg.meta["d1"], gg.meta["d2"])
+        assert run(G, gi.query("C4"))[0] == cf.cycle4(gg)
+    finally:
+        G.free()
+
+
+def test_candidate_counts_match_cpu_predicate():
+    """K1 filter: |C(u)| = #{v : label(v) = label_Q(u) and deg(v) >= deg_Q(u)}."""
+    g = gi.rmat(12, 8, seed=9).with_labels(gi.uniform_labels(4096, 4, 9))
+    deg = np.diff(g.offsets)
+    G = load(g)
+    try:
+        for qname, ql in [("S3", [0, 1, 2, 3]), ("house", [1, 1, 2, 3, 0]), ("K4", None)]:
+            q = gi.query(qname, ql)
+            _, _, r = run(G, q)
+            qdeg = np.zeros(q.num_nodes, int)
+            for a, b in q.edges:
+                qdeg[a] += 1
+                qdeg[b] += 1
+            for u in range(q.num_nodes):
+                lab_ok = np.ones(g.num_nodes, bool) if ql is None else (g.labels == ql[u])
+                assert r.candidates[u] == int(np.sum(lab_ok & (deg >= qdeg[u]))), (qname, u)
+    finally:
+        G.free()
+
+
+def test_chunking_invariance():
+    """Tiny memory budgets force many chunks per level; results must not change."""
+    g = gi.rmat(11, 16, seed=2)
+    G = load(g)
+    try:
+        for qname in ["K4", "C4", "house"]:
+            q = gi.query(qname)
+            cnt, ref = oracle.match(g, q)
+            for budget in (64 << 10, 1 << 20, 0):
+                c, rows, r = run(G, q, "enumerate", mem_budget_bytes=budget)
+                assert c == cnt
+                assert_rows_equal(rows, ref, f"{qname} budget {budget}")
+                c2, _, r2 = run(G, q, "count", mem_budget_bytes=budget)
+                assert c2 == cnt
+            assert r.num_chunks >= 1
+    finally:
+        G.free()
+
+
+def test_shard_invariance():
+    """P root shards run sequentially on one GPU: counts add up, rows union = all rows."""
+    g = gi.rmat(11, 16, seed=3).with_labels(gi.uniform_labels(2048, 2, 3))
+    G = load(g)
+    try:
+        for q in [gi.query("K3"), gi.query("P4", [0, 1, 1, 0]), gi.query("K4")]:
+            cnt, ref = oracle.match(g, q)
+            for P in (2, 3, 8):
+                tot = 0
+                parts = []
+                for s in range(P):
+                    c, rows, _ = run(G, q, "enumerate", shard_index=s, num_shards=P)
+                    tot += c
+                    parts.append(rows)
+                assert tot == cnt
+                assert_rows_equal(oracle.sort_rows(np.concatenate(parts)), ref, f"{q.name} P={P}")
+    finally:
+        G.free()
+
+
+def test_root_subset_sampling():
+    g = gi.rmat(12, 16, seed=6).with_labels(gi.uniform_labels(4096, 3, 6))
+    G = load(g)
+    try:
+        rng = np.random.default_rng(1)
+        roots = np.unique(rng.integers(0, 4096, 300)).astype(np.int32)
+        for q in [gi.query("house", [0, 1, 2, 0, 1]), gi.query("K3"), gi.query("C4", [0, 1, 0, 1])]:
+            cnt, ref = oracle.match(g, q, roots=roots)
+            c, rows, _ = run(G, q, "enumerate", root_subset=roots)
+            assert c == cnt
+            assert_rows_equal(rows, ref, q.name)
+    finally:
+        G.free()
+
+
+def test_relabel_invariance():
+    g = gi.rmat(10, 8, seed=8)
+    perm = np.random.default_rng(3).permutation(g.num_nodes).astype(np.int32)
+    src = np.repeat(np.arange(g.num_nodes), np.diff(g.offsets))
+    g2 = gi.csr_from_edges(g.num_nodes, perm[src], perm[g.cols])
+    G1, G2 = load(g), load(g2)
+    try:
+        for qname in ["K3", "C4", "P4"]:
+            q = gi.query(qname)
+            _, r1, _ = run(G1, q, "enumerate")
+            _, r2, _ = run(G2, q, "enumerate")
+            assert_rows_equal(oracle.sort_rows(perm[r1]), r2, qname)
+    finally:
+        G1.free()
+        G2.free()
+
+
+def test_edge_cases():
+    # single vertex query -> n; K2 -> 2m; k > n -> 0; label absent -> 0
+    g = gi.random_gnp(20, 1, 4, 1)
+    G = load(g)
+    try:
+        assert run(G, gi.Query(1, [], None))[0] == 20
+        c, rows, _ = run(G, gi.Query(1, [], None), "enumerate")
+        assert rows[:, 0].tolist() == list(range(20))
+        assert run(G, gi.query("K2"))[0] == 2 * g.num_edges
+        with pytest.raises(gsm.GsmError) as e:
+            run(G, gi.Query(3, [(0, 1)], None))
+        assert e.value.status == 3  # disconnected query
+        with pytest.raises(gsm.GsmError) as e:
+            run(G, gi.query("K3", [0, 0, 0]))
+        assert e.value.status == 1  # labels on an unlabeled graph
+        with pytest.raises(gsm.GsmError):
+            run(G, gi.Query(3, [(0, 1), (1, 1)], None))  # self-loop in Q
+        with pytest.raises(gsm.GsmError):
+            run(G, gi.Query(33, [(i, i + 1) for i in range(32)], None))  # k > 32
+    finally:
+        G.free()
+    G = load(gi.complete(4))
+    try:
+        assert run(G, gi.query("C5"))[0] == 0  # k > n
+    finally:
+        G.free()
+    gl = gi.complete(5).with_labels(np.array([1, 1, 2, 2, 2], np.uint32))
+    G = load(gl)
+    try:
+        assert run(G, gi.query("K3", [1, 2, 7]))[0] == 0
+        c, rows, _ = run(G, gi.query("K3", [1, 2, 7]), "enumerate")
+        assert c == 0 and rows.shape[0] == 0
+    finally:
+        G.free()
+    # graph without edges, isolated vertices
+    ge = gi.csr_from_edges(10, np.zeros(0, np.int32), np.zeros(0, np.int32))
+    G = load(ge)
+    try:
+        assert run(G, gi.query("K2"))[0] == 0
+        assert run(G, gi.Query(1, [], None))[0] == 10
+    finally:
+        G.free()
+
+
+def test_invalid_graphs_rejected():
+    g = gi.complete(4)
+    bad_unsorted = g.cols.copy()
+    bad_unsorted[0], bad_unsorted[1] = bad_unsorted[1], bad_unsorted[0]
+    cases = [
+        (g.offsets, bad_unsorted),
+        (g.offsets, np.where(g.cols == 3, 9, g.cols).astype(np.int32)),  # out of range
+    ]
+    # asymmetric: drop one direction
+    off = np.array([0, 1, 1], np.int64)
+    cases.append((off, np.array([1], np.int32)))
+    # self-loop
+    cases.append((np.array([0, 1], np.int64), np.array([0], np.int32)))
+    for o, c in cases:
+        with pytest.raises(gsm.GsmError) as e:
+            gsm.gsm_load_graph(len(o) - 1, o, c, validate=True)
+        assert e.value.status == 2
+    with pytest.raises(gsm.GsmError) as e:
+        gsm.gsm_load_graph(0, np.zeros(1, np.int64), np.zeros(0, np.int32))
+    assert e.value.status == 2
+
+
+def test_device_pointer_load_and_profile():
+    import torch
+    g = gi.rmat(12, 8, seed=1)
+    off = torch.from_numpy(g.offsets).cuda()
+    cols = torch.from_numpy(g.cols).cuda()
+    G = gsm.gsm_load_graph(g.num_nodes, off, cols, None, device=0, validate=True)
+    try:
+        c, _, r = run(G, gi.query("K3"), flags=gsm.GSM_FLAG_PROFILE)
+        assert c == 6 * oracle.count_triangles(g)
+        assert r.prof["expand"]["launches"] >= 1 and r.prof["expand"]["ms"] > 0
+        assert r.prof["expand"]["alg_bytes"] > 0 and r.prof["filter"]["ms"] > 0
+        rt = run(G, gi.query("K3"), "enumerate")[1]
+        _, _, re = run(G, gi.query("K3"), "enumerate")
+        t = re.rows_torch()
+        assert t.is_cuda and t.shape[0] == c
+        assert np.array_equal(t.cpu().numpy(), rt)
+        re.free()
+    finally:
+        G.free()

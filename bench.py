@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""bench.py — device-timed GSM hot path (BASELINE.json metric: embeddings/s and
+query ms at 1/2/4/8 B200; achieved HBM GB/s vs peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload rmat24] [--impl ours|reference]
+
+A step = one pass of the whole hot path over the workload: gsm_match (COUNT,
+all embeddings) of every query of the workload on the resident data graph
+(filter -> roots -> per-position plan/scan/partition/expand -> count).  Default
+workload = BASELINE configs[4] (R-MAT-24, K3 + K4, chunked frontier), the
+configuration the metric is quoted on at 1/2/4/8 GPUs.  Multi-GPU: one process
+per GPU (torchrun), data graph replicated (each rank regenerates it), root
+candidates sharded round-robin by (degree, id) rank, one NCCL all-reduce of
+the counts per step; time = max over ranks.
+
+--impl reference: the CPU oracle (oracle/, plain DFS) timed on this host's
+cores on a bounded root sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--workload", default=os.environ.get("GSM_BENCH_WORKLOAD", "rmat24"))
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        pg = dist
+    return world, rank, local, pg
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def ncu_traffic(workload: str):
+    """Per-launch DRAM bytes of the expand kernel from the committed ncu summary (or None)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(path))
+        e = d.get(workload, {}).get("k_expand")
+        return None if e is None else e.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------- oracle baseline
+def oracle_sample(g, queries, budget_s: float, rank_roots=None):
+    """Calibrate an evenly strided root sample so the oracle spends ~budget_s seconds;
+    returns (roots, embeddings, seconds, threads).  All embeddings with f(0) in roots."""
+    import numpy as np
+    import oracle
+
+    n = g.num_nodes
+    stride = max(1, n // 64)
+    while True:
+        roots = np.arange(stride // 2, n, stride, dtype=np.int32)
+        t0 = time.perf_counter()
+        tot = 0
+        for q in queries:
+            tot += oracle.match(g, q, roots=roots, count_only=True)[0]
+        dt = time.perf_counter() - t0
+        if dt >= budget_s / 4 or stride == 1:
+            if dt < budget_s / 2 and stride > 1:
+                stride = max(1, int(stride * dt / budget_s))
+                continue
+            return roots, tot, dt, oracle.num_threads()
+        stride = max(1, stride // 8 if dt < budget_s / 64 else stride // 2)
+
+
+def cpu_baseline(g, w, budget_s):
+    roots, tot, dt, threads = oracle_sample(g, w.queries, budget_s)
+    return {"value": tot / dt if dt > 0 else None, "unit": "embeddings/s", "cores": threads, "kind": "oracle",
+            "sample": f"all embeddings of {[q.name for q in w.queries]} with f(query vertex 0) in an evenly strided "
+                      f"sample of {len(roots)} of {g.num_nodes} vertices; {tot} embeddings in {dt:.2f} s"}
+
+
+def run_reference(args, world, rank):
+    import oracle  # noqa: F401  (reference arm = the CPU oracle)
+    from gsm_inputs import workloads
+
+    if rank != 0:
+        return
+    w = workloads.get(args.workload)
+    g = w.graph()
+    per_step = max(1.0, min(8.0, 120.0 / max(1, args.steps + args.warmup)))
+    roots, _, _, threads = oracle_sample(g, w.queries, per_step)
+    import oracle as O
+    for _ in range(args.warmup):
+        for q in w.queries:
+            O.match(g, q, roots=roots, count_only=True)
+    t0 = time.perf_counter()
+    tot = 0
+    for _ in range(args.steps):
+        for q in w.queries:
+            tot += O.match(g, q, roots=roots, count_only=True)[0]
+    dt = time.perf_counter() - t0
+    value = tot / dt
+    sample = (f"all embeddings of {[q.name for q in w.queries]} with f(query vertex 0) in an evenly strided sample "
+              f"of {len(roots)} of {g.num_nodes} vertices per step")
+    out = {"impl": "reference", "metric": "embeddings/s", "value": value, "unit": "embeddings/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+           "data": "synthetic", "config": config_of(w, g),
+           "cpu_baseline": {"value": value, "unit": "embeddings/s", "cores": threads, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "embeddings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def config_of(w, g):
+    return {"workload": f"{w.name} (BASELINE configs[{w.config_index}]): {w.description}",
+            "graph": {"name": g.name, "num_nodes": g.num_nodes, "directed_edges": g.nnz,
+                      "csr_bytes": int(g.offsets.nbytes + g.cols.nbytes + (0 if g.labels is None else g.labels.nbytes))},
+            "queries": [q.name for q in w.queries], "mode": "count, all embeddings (= |Aut(Q)| x orbit representatives)",
+            "mem_budget_bytes": w.mem_budget_bytes,
+            "l2": "inputs larger than L2 (no flush)" if g.offsets.nbytes + g.cols.nbytes > 126e6
+                  else "graph smaller than L2: L2 flushed (256 MiB write) before every timed step"}
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, world, rank, local, dist):
+    import numpy as np
+    import torch
+
+    from gsm_inputs import workloads
+    from paper_2003_01527_b200 import gsm
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = workloads.get(args.workload)
+    g = w.graph()
+    G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=local)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    graph_bytes = g.offsets.nbytes + g.cols.nbytes
+    flush = None
+    if graph_bytes <= 126e6:
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(flags, G_=None):
+        G_ = G_ or G
+        tot_all = tot_unique = launches = 0
+        profs = []
+        for q in w.queries:
+            r = gsm.gsm_match(G_, q.num_nodes, q.edges, q.labels, mode=gsm.GSM_MODE_COUNT, flags=flags,
+                              shard_index=rank, num_shards=world, mem_budget_bytes=w.mem_budget_bytes, stream=sptr)
+            tot_all += r.count
+            tot_unique += r.count_unique
+            launches += r.kernel_launches
+            profs.append(r.prof)
+        return tot_all, tot_unique, launches, profs
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        if flush is not None:
+            flush.zero_()
+        step(gsm.GSM_FLAG_PROFILE)
+    barrier()
+    ms_steps = []
+    counts = None
+    launches = 0
+    prof_tot = {}
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            c_all, c_uni, nl, profs = step(gsm.GSM_FLAG_PROFILE)
+            ev1.record(stream)
+            ev1.synchronize()
+            ms_steps.append(ev0.elapsed_time(ev1))
+            counts = (c_all, c_uni)
+            launches += nl
+            for p in profs:
+                for kname, d in p.items():
+                    t = prof_tot.setdefault(kname, {"launches": 0, "ms": 0.0, "alg_bytes": 0.0})
+                    for key in t:
+                        t[key] += d[key]
+    barrier()
+    ms = sum(ms_steps) / len(ms_steps)
+    c_all, c_uni = counts
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([c_all, c_uni, launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(c)
+        c_all, c_uni, launches = (int(x) for x in c.tolist())
+
+    # ---- end to end through the C ABI with host buffers (pinned), per step:
+    #      H2D CSR + relabel (gsm_load_graph) + matches + D2H counts + gsm_free
+    e2e = None
+    if args.e2e_steps > 0:
+        off_h = torch.from_numpy(g.offsets).pin_memory()
+        cols_h = torch.from_numpy(g.cols).pin_memory()
+        lab_h = None if g.labels is None else torch.from_numpy(g.labels.view(np.int32)).pin_memory()
+        barrier()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        e_cnt = 0
+        for _ in range(args.e2e_steps):
+            G2 = gsm.gsm_load_graph(g.num_nodes, off_h, cols_h, lab_h, device=local, stream=sptr)
+            e_cnt = step(0, G2)[0]
+            G2.free()
+        ev1.record(stream)
+        ev1.synchronize()
+        e_ms = ev0.elapsed_time(ev1) / args.e2e_steps
+        if dist is not None:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+            c = torch.tensor([e_cnt], dtype=torch.int64, device=dev)
+            dist.all_reduce(c)
+            e_cnt = int(c.item())
+        h2d = (g.offsets.nbytes + g.cols.nbytes + (0 if g.labels is None else g.labels.nbytes)) * world
+        e2e = {"value": e_cnt / (e_ms / 1000.0), "unit": "embeddings/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * len(w.queries) * world)}
+    G.free()
+
+    if rank != 0:
+        return
+    peaks = load_peaks()
+    ex = prof_tot.get("expand", {"ms": 0, "alg_bytes": 0, "launches": 0})
+    # dominant kernel = the one with the largest share of device time
+    dom = max(prof_tot.items(), key=lambda kv: kv[1]["ms"])[0] if prof_tot else "expand"
+    kp = prof_tot.get(dom, ex)
+    achieved = (kp["alg_bytes"] / (kp["ms"] / 1e3)) / 1e9 if kp["ms"] > 0 else None
+    peak = peaks.get("hbm_gbs")
+    traffic = ncu_traffic(args.workload) if dom == "expand" else None
+    roof = {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if (achieved and peak) else None,
+            "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peak else "absent",
+            "launches_per_step": kp["launches"] / args.steps,
+            "kernel_ms_per_step": kp["ms"] / args.steps,
+            "alg_bytes_per_launch": kp["alg_bytes"] / max(1, kp["launches"]),
+            "share_of_step": (kp["ms"] / args.steps) / ms if ms > 0 else None,
+            "per_kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof_tot.items()}}
+    out = {"metric": "embeddings/s", "value": c_all / (ms / 1000.0), "unit": "embeddings/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+           "config": config_of(w, g),
+           "counts_per_step": {"all": c_all, "unique": c_uni},
+           "unique_per_s": c_uni / (ms / 1000.0),
+           "query_ms": ms, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(g, w, args.cpu_seconds)
+        except Exception as e:  # baseline failure must not hide the measurement
+            out["cpu_baseline"] = {"value": None, "error": repr(e)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse_args()
+    world, rank, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

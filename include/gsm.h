@@ -225,6 +225,15 @@ typedef struct {
 
 GSM_API gsm_status gsm_plan_query(const gsm_query* q, const uint64_t* cand, uint32_t flags, gsm_plan_info* out);
 
+/*
+ * gsm_sort_rows — lexicographic (unsigned tuple) in-place sort of num_rows x width int32 rows
+ * in DEVICE memory on `device`, values in [0, max_id].  Used to merge the enumerated row
+ * shards of several GPUs; the same LSD radix sort gsm_match uses to order its
+ * output.  Synchronous on `stream` (NULL = legacy default stream).
+ */
+GSM_API gsm_status gsm_sort_rows(int32_t* rows, uint64_t num_rows, int32_t width, int64_t max_id, int32_t device,
+                                 void* stream);
+
 /* Thread-local message for the last non-OK status ("" if none). */
 GSM_API const char* gsm_last_error(void);
 

@@ -241,8 +241,9 @@ __global__ void __launch_bounds__(kThreads) k_plan_rows(const int32_t* __restric
         if (lov + 1 >= hiv || blen <= 0) {
             bt = bs;
         } else if (blen > 8) {
-            if (lov > ba) bs = lower_bound_cols(cols, bs, bt, lov + 1);
-            if (hiv < ba) bt = lower_bound_cols(cols, bs, bt, hiv);
+            // exact segment: bounds equal to the pivot itself are already exact via up[a]
+            if (lov >= 0 && lov != ba) bs = lower_bound_cols(cols, bs, bt, lov + 1);
+            if (hiv < n && hiv != ba) bt = lower_bound_cols(cols, bs, bt, hiv);
         }
         rbeg[r] = bs;
         rlen[r] = bt > bs ? bt - bs : 0;

@@ -507,6 +507,37 @@ gsm_status gsm_result_copy_rows(const gsm_result* r, int32_t* dst, int32_t dst_o
     return GSM_OK;
 }
 
+gsm_status gsm_sort_rows(int32_t* rows, uint64_t num_rows, int32_t width, int64_t max_id, int32_t device,
+                         void* stream) {
+    if (num_rows == 0) return GSM_OK;
+    if (!rows || width < 1 || max_id < 0) {
+        gsm::set_error("bad arguments to gsm_sort_rows");
+        return GSM_ERR_INVALID_ARGUMENT;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    try {
+        gsm::clear_error();
+        GSM_CUDA(cudaSetDevice(device));
+        cudaStream_t s = (cudaStream_t)stream;
+        gsm::DevBuf<int32_t> tmp;
+        tmp.ensure((size_t)num_rows * width, s);
+        gsm::sort_rows(rows, (int64_t)num_rows, width, max_id + 1, tmp.p, s);
+        GSM_CUDA(cudaMemcpyAsync(rows, tmp.p, sizeof(int32_t) * num_rows * width, cudaMemcpyDeviceToDevice, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        cudaSetDevice(prev);
+        return GSM_OK;
+    } catch (const gsm::Failure& f) {
+        cudaSetDevice(prev);
+        gsm::set_error(f.msg);
+        return f.status;
+    } catch (...) {
+        cudaSetDevice(prev);
+        gsm::set_error("unexpected exception in gsm_sort_rows");
+        return GSM_ERR_CUDA;
+    }
+}
+
 gsm_status gsm_plan_query(const gsm_query* q, const uint64_t* cand, uint32_t flags, gsm_plan_info* out) {
     if (!out) {
         gsm::set_error("out is NULL");

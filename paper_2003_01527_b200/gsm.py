@@ -79,7 +79,7 @@ class gsm_plan_info(ctypes.Structure):
 _lib = None
 
 EXPORTS = ["gsm_load_graph", "gsm_free", "gsm_graph_info", "gsm_match", "gsm_result_free", "gsm_result_copy_rows",
-           "gsm_plan_query", "gsm_last_error", "gsm_version"]
+           "gsm_plan_query", "gsm_sort_rows", "gsm_last_error", "gsm_version"]
 
 
 def lib():
@@ -98,6 +98,7 @@ def lib():
         L.gsm_result_free.argtypes = [ctypes.POINTER(gsm_result)]
         L.gsm_result_copy_rows.argtypes = [ctypes.POINTER(gsm_result), P, i32]
         L.gsm_plan_query.argtypes = [ctypes.POINTER(gsm_query), P, ctypes.c_uint32, ctypes.POINTER(gsm_plan_info)]
+        L.gsm_sort_rows.argtypes = [P, ctypes.c_uint64, i32, i64, i32, P]
         L.gsm_last_error.restype = ctypes.c_char_p
         L.gsm_version.restype = ctypes.c_char_p
         for name in EXPORTS:
@@ -254,6 +255,15 @@ def gsm_result_copy_rows(res: Result, dst, dst_on_device: bool):
     p, _, keep = _ptr(dst)
     _check(lib().gsm_result_copy_rows(ctypes.byref(res.raw), p, 1 if dst_on_device else 0))
     del keep
+
+
+def gsm_sort_rows(rows, max_id: int, stream: Optional[int] = None):
+    """In-place lexicographic sort of a CUDA int32 tensor (num_rows x width), values in [0, max_id]."""
+    if not (hasattr(rows, "is_cuda") and rows.is_cuda and rows.is_contiguous() and rows.dim() == 2):
+        raise ValueError("gsm_sort_rows needs a contiguous 2-D CUDA int32 tensor")
+    _check(lib().gsm_sort_rows(ctypes.c_void_p(rows.data_ptr()), rows.shape[0], rows.shape[1], int(max_id),
+                               rows.device.index or 0, stream))
+    return rows
 
 
 def gsm_plan_query(num_nodes: int, edges: Sequence, labels=None, candidates=None, flags: int = 0) -> dict:

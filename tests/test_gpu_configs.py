@@ -1,0 +1,185 @@
+"""GPU parity on the five BASELINE.json configs at full size.
+
+Full sorted row lists vs the oracle where the oracle finishes (configs 0-2);
+for configs 3-4 (R-MAT-22 house, R-MAT-24 K3/K4): root-sampled oracle parity
+(exercises the direct search), exact counts from independent counters, and
+the symmetry identities that pin the production (ID-constrained) path:
+count_all = |Aut| x count_unique = count of the direct search."""
+import numpy as np
+import pytest
+
+import gsm_inputs as gi
+import oracle
+from gsm_inputs import workloads
+from oracle import closed_forms as cf
+from paper_2003_01527_b200 import gsm
+
+from gpu_helpers import assert_rows_equal, is_sorted_unique, load, run
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config0_er1000_triangle(seed):
+    g = gi.erdos_renyi(1000, 4000, seed)
+    q = gi.query("K3")
+    G = load(g)
+    try:
+        cnt, ref = oracle.match(g, q)
+        c, rows, _ = run(G, q, "enumerate")
+        assert c == cnt == cf.triangle_trace(cf.dense_adj(g))
+        assert_rows_equal(rows, ref, "er1000 all")
+        cu, rowsu, _ = run(G, q, "enumerate", flags=gsm.GSM_FLAG_UNIQUE)
+        aut = oracle.automorphisms(q)
+        assert cu * 6 == cnt
+        assert_rows_equal(oracle.unique(rowsu, aut), oracle.unique(ref, aut), "er1000 unique")
+    finally:
+        G.free()
+
+
+@pytest.fixture(scope="module")
+def rmat16():
+    w = workloads.get("rmat16")
+    g = w.graph()
+    G = load(g)
+    yield w, g, G
+    G.free()
+
+
+@pytest.mark.parametrize("qi", [0, 1, 2, 3])
+def test_config1_rmat16_labeled_path_and_star(rmat16, qi):
+    w, g, G = rmat16
+    q = w.queries[qi]
+    if q.name.startswith("P4"):
+        closed = cf.path4_labeled_vectorised(g, *q.labels, num_labels=8)
+    else:
+        closed = cf.star_vectorised(g, q.labels[0], q.labels[1:], 8)
+    c_count, _, r = run(G, q, "count")
+    assert c_count == closed, (q.name, c_count, closed)
+    cnt, ref = oracle.match(g, q)
+    assert cnt == closed
+    c, rows, _ = run(G, q, "enumerate")
+    assert c == cnt
+    assert_rows_equal(rows, ref, q.name)
+    del rows, ref
+    cu, _, ru = run(G, q, "count", flags=gsm.GSM_FLAG_UNIQUE)
+    assert cu * ru.automorphisms == cnt
+
+
+@pytest.fixture(scope="module")
+def grid1m():
+    w = workloads.get("grid1m")
+    g = w.graph()
+    G = load(g)
+    yield w, g, G
+    G.free()
+
+
+def test_config2_grid_k4(grid1m):
+    w, g, G = grid1m
+    q = gi.query("K4")
+    c, rows, _ = run(G, q, "enumerate")
+    assert c == cf.grid_diag_k4(g.meta["d2"])
+    cnt, ref = oracle.match(g, q)
+    assert c == cnt
+    assert_rows_equal(rows, ref, "grid K4")
+    assert run(G, gi.query("K3"))[0] == cf.grid_diag_k3(g.meta["d1"], g.meta["d2"])
+
+
+def test_config2_grid_c4(grid1m):
+    w, g, G = grid1m
+    q = gi.query("C4")
+    c, rows, _ = run(G, q, "enumerate")
+    cnt, ref = oracle.match(g, q)
+    assert c == cnt == cf.cycle4(g)
+    assert_rows_equal(rows, ref, "grid C4")
+    assert is_sorted_unique(rows)
+
+
+@pytest.fixture(scope="module")
+def rmat22():
+    w = workloads.get("rmat22")
+    g = w.graph()
+    G = load(g, validate=True)
+    yield w, g, G
+    G.free()
+
+
+def _root_sample(g, label, n_uniform, seed):
+    """Uniform sample of label-matching vertices + 16 moderately high-degree ones
+    (around the 99.9th degree percentile: hubs make the plain DFS infeasible)."""
+    rng = np.random.default_rng(seed)
+    cand = np.nonzero(g.labels == label)[0] if label is not None else np.arange(g.num_nodes)
+    uni = rng.choice(cand, size=min(n_uniform, len(cand)), replace=False)
+    deg = np.diff(g.offsets)[cand]
+    order = cand[np.argsort(deg, kind="stable")]
+    hi = order[int(len(order) * 0.999): int(len(order) * 0.999) + 16]
+    return np.unique(np.concatenate([uni, hi])).astype(np.int32)
+
+
+@pytest.mark.parametrize("qi", [0, 1])
+def test_config3_rmat22_house(rmat22, qi):
+    w, g, G = rmat22
+    q = w.queries[qi]
+    c_all, _, r = run(G, q, "count")
+    c_uni, _, ru = run(G, q, "count", flags=gsm.GSM_FLAG_UNIQUE)
+    c_direct, _, _ = run(G, q, "count", flags=gsm.GSM_FLAG_NO_SYMMETRY)
+    aut = oracle.automorphisms(q)
+    assert r.automorphisms == len(aut)
+    assert c_all == len(aut) * c_uni == c_direct
+    assert c_all > 0
+    roots = _root_sample(g, q.labels[0], 4096, 7 + qi)
+    cnt, ref = oracle.match(g, q, roots=roots)
+    c, rows, _ = run(G, q, "enumerate", root_subset=roots)
+    assert c == cnt and cnt > 0
+    assert_rows_equal(rows, ref, q.name + " root sample")
+
+
+@pytest.fixture(scope="module")
+def rmat24():
+    w = workloads.get("rmat24")
+    g = w.graph()
+    G = load(g)
+    yield w, g, G
+    G.free()
+
+
+def test_config4_rmat24_triangles_exact(rmat24):
+    w, g, G = rmat24
+    q = gi.query("K3")
+    c, _, r = run(G, q, "count", mem_budget_bytes=w.mem_budget_bytes)
+    T = oracle.count_triangles(g)
+    assert c == 6 * T
+    # shard invariance: 4 shards sequentially on one GPU
+    tot = sum(run(G, q, "count", shard_index=s, num_shards=4, mem_budget_bytes=w.mem_budget_bytes)[0]
+              for s in range(4))
+    assert tot == c
+
+
+def test_config4_rmat24_k4_sampled_and_identities(rmat24):
+    w, g, G = rmat24
+    q = gi.query("K4")
+    c_all, _, r = run(G, q, "count", mem_budget_bytes=w.mem_budget_bytes)
+    c_uni, _, _ = run(G, q, "count", flags=gsm.GSM_FLAG_UNIQUE, mem_budget_bytes=w.mem_budget_bytes)
+    assert c_all == 24 * c_uni and c_all > 0
+    assert r.num_chunks > 1  # the fixed budget forces a chunked frontier
+    roots = _root_sample(g, None, 4096, 11)
+    cnt, ref = oracle.match(g, q, roots=roots)
+    c, rows, _ = run(G, q, "enumerate", root_subset=roots)
+    assert c == cnt
+    assert_rows_equal(rows, ref, "rmat24 K4 root sample")
+    cnt3, ref3 = oracle.match(g, gi.query("K3"), roots=roots)
+    c3, rows3, _ = run(G, gi.query("K3"), "enumerate", root_subset=roots)
+    assert c3 == cnt3
+    assert_rows_equal(rows3, ref3, "rmat24 K3 root sample")
+
+
+def test_config4_k4_exact_at_scale20():
+    """K4 exact count against the independent CPU counter where it finishes (scale 20)."""
+    g = gi.rmat(20, 16, 1)
+    G = load(g)
+    try:
+        c, _, _ = run(G, gi.query("K4"), mem_budget_bytes=1 << 30)
+        assert c == 24 * oracle.count_k4(g)
+    finally:
+        G.free()

@@ -101,8 +101,8 @@ def test_named_queries_on_random_graphs(qname):
     for seed in (1, 2):
         g = gi.random_gnp(60, 1, 6, seed)
         check_all_modes(g, gi.query(qname), what=f"{qname} s{seed}")
-    g = gi.rmat(10, 8, seed=4)
-    check_all_modes(g, gi.query(qname), what=f"{qname} rmat10")
+    g = gi.rmat(8, 8, seed=4)
+    check_all_modes(g, gi.query(qname), what=f"{qname} rmat8")
 
 
 def test_labeled_named_queries():
@@ -164,10 +164,10 @@ def test_candidate_counts_match_cpu_predicate():
 
 def test_chunking_invariance():
     """Tiny memory budgets force many chunks per level; results must not change."""
-    g = gi.rmat(11, 16, seed=2)
+    g = gi.rmat(9, 8, seed=2)
     G = load(g)
     try:
-        for qname in ["K4", "C4", "house"]:
+        for qname in ["K4", "C4", "diamond"]:
             q = gi.query(qname)
             cnt, ref = oracle.match(g, q)
             for budget in (64 << 10, 1 << 20, 0):
@@ -177,13 +177,15 @@ def test_chunking_invariance():
                 c2, _, r2 = run(G, q, "count", mem_budget_bytes=budget)
                 assert c2 == cnt
             assert r.num_chunks >= 1
+            r_small = run(G, q, "count", mem_budget_bytes=64 << 10)[2]
+            assert r_small.num_chunks > r.num_chunks  # the small budget really chunks
     finally:
         G.free()
 
 
 def test_shard_invariance():
     """P root shards run sequentially on one GPU: counts add up, rows union = all rows."""
-    g = gi.rmat(11, 16, seed=3).with_labels(gi.uniform_labels(2048, 2, 3))
+    g = gi.rmat(10, 8, seed=3).with_labels(gi.uniform_labels(1024, 2, 3))
     G = load(g)
     try:
         for q in [gi.query("K3"), gi.query("P4", [0, 1, 1, 0]), gi.query("K4")]:

@@ -52,6 +52,11 @@ WORKLOADS = {
     "rmat24": Workload("rmat24", 4, "R-MAT-24 ef16 unlabeled; K3, K4 (16 GiB frontier budget)",
                        lambda: gi.rmat(24, 16, 1), [gi.query("K3"), gi.query("K4")],
                        mem_budget_bytes=16 << 30),
+    # development workloads (not BASELINE configs)
+    "rmat20": Workload("rmat20", -1, "R-MAT-20 ef16 unlabeled; K3, K4", lambda: gi.rmat(20, 16, 1),
+                       [gi.query("K3"), gi.query("K4")], mem_budget_bytes=4 << 30),
+    "rmat24_k3": Workload("rmat24_k3", 4, "R-MAT-24 ef16 unlabeled; K3 only", lambda: gi.rmat(24, 16, 1),
+                          [gi.query("K3")], mem_budget_bytes=16 << 30),
 }
 
 

@@ -212,48 +212,72 @@ __device__ __forceinline__ int64_t lower_bound_cols(const int32_t* __restrict__ 
     return lo;
 }
 
+// Admissible segment of N(a) for candidates in the open interval (lov, hiv):
+// up[a] splits the sorted list at a itself (exact when a bound equals a);
+// otherwise an optional binary search makes it exact.
+__device__ __forceinline__ void admissible_segment(const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                                                   const int32_t* __restrict__ up, int64_t n, int32_t a,
+                                                   int64_t lov, int64_t hiv, bool refine, int64_t& s,
+                                                   int64_t& t) {
+    s = off[a];
+    t = off[a + 1];
+    if (lov >= a || hiv <= a) {
+        const int64_t split = s + up[a];
+        if (lov >= a) s = split;
+        if (hiv <= a) t = split;
+    }
+    if (refine) {
+        if (lov >= 0 && lov != a) s = lower_bound_cols(cols, s, t, lov + 1);
+        if (hiv < n && hiv != a) t = lower_bound_cols(cols, s, t, hiv);
+    }
+    if (t < s) t = s;
+}
+
 __global__ void __launch_bounds__(kThreads) k_plan_rows(const int32_t* __restrict__ F, int64_t R, LevelPlan L,
                                                         const int64_t* __restrict__ off,
                                                         const int32_t* __restrict__ cols,
                                                         const int32_t* __restrict__ up, int64_t n,
                                                         int64_t* __restrict__ rbeg, int64_t* __restrict__ rlen,
-                                                        uint8_t* __restrict__ rpiv) {
+                                                        uint8_t* __restrict__ rpiv, int64_t* __restrict__ cbeg,
+                                                        int32_t* __restrict__ clen) {
     const int W = L.width;
+    const int nb = L.nb;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
         const int32_t* row = F + r * W;
         int64_t lov = -1, hiv = n;
         for (int q = 0; q < L.nlo; ++q) lov = max(lov, (int64_t)row[L.lo[q]]);
         for (int q = 0; q < L.nhi; ++q) hiv = min(hiv, (int64_t)row[L.hi[q]]);
-        int64_t bs = 0, bt = 0, blen = INT64_MAX;
+        const bool empty = lov + 1 >= hiv;
+        // pivot = shortest estimated segment (up-split only, no search yet)
+        int64_t blen = INT64_MAX;
         int bq = 0;
-        int32_t ba = 0;
-        for (int q = 0; q < L.nb; ++q) {
-            const int32_t a = row[L.bpos[q]];
-            int64_t s0 = off[a], t0 = off[a + 1];
-            if (lov >= a || hiv <= a) {
-                const int64_t split = s0 + up[a];
-                if (lov >= a) s0 = split;
-                if (hiv <= a) t0 = split;
-            }
-            const int64_t len = t0 - s0;
-            if (len < blen) { blen = len; bs = s0; bt = t0; bq = q; ba = a; }
+        for (int q = 0; q < nb; ++q) {
+            int64_t s0, t0;
+            admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, false, s0, t0);
+            if (t0 - s0 < blen) { blen = t0 - s0; bq = q; }
         }
-        if (lov + 1 >= hiv || blen <= 0) {
-            bt = bs;
-        } else if (blen > 8) {
-            // exact segment: bounds equal to the pivot itself are already exact via up[a]
-            if (lov >= 0 && lov != ba) bs = lower_bound_cols(cols, bs, bt, lov + 1);
-            if (hiv < n && hiv != ba) bt = lower_bound_cols(cols, bs, bt, hiv);
+        // exact segments: the pivot's (its length is the work of this row) and the
+        // membership lists of the other backward neighbours (searched per candidate)
+        int64_t ps = 0, pt = 0;
+        for (int q = 0; q < nb; ++q) {
+            int64_t s0, t0;
+            const bool pivot = q == bq;
+            admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, !empty && (pivot ? blen > 8 : true),
+                               s0, t0);
+            if (empty) t0 = s0;
+            cbeg[r * nb + q] = s0;
+            clen[r * nb + q] = (int32_t)(t0 - s0);
+            if (pivot) { ps = s0; pt = t0; }
         }
-        rbeg[r] = bs;
-        rlen[r] = bt > bs ? bt - bs : 0;
+        rbeg[r] = ps;
+        rlen[r] = pt - ps;
         rpiv[r] = (uint8_t)bq;
     }
 }
 
 void launch_plan_rows(const DevGraph& g, const int32_t* F, int64_t R, const LevelPlan& L, int64_t* rbeg,
-                      int64_t* rlen, uint8_t* rpiv, cudaStream_t s) {
-    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, g.cols, g.up, g.n, rbeg, rlen, rpiv);
+                      int64_t* rlen, uint8_t* rpiv, int64_t* cbeg, int32_t* clen, cudaStream_t s) {
+    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, g.cols, g.up, g.n, rbeg, rlen, rpiv, cbeg, clen);
     GSM_LAUNCH("k_plan_rows");
 }
 
@@ -312,9 +336,8 @@ void launch_partition(const int64_t* P, int64_t R, int64_t S, int64_t D0, int64_
 // One CTA per merge-path tile (grid-stride); the tile's rows (entries, pivot
 // segment start, work offsets) are staged in shared memory first.
 // ============================================================================
-__device__ __forceinline__ bool in_list(const int64_t* __restrict__ off, const int32_t* __restrict__ cols, int32_t a,
-                                        int32_t v, unsigned& probes) {
-    int64_t lo = off[a], hi = off[a + 1];
+__device__ __forceinline__ bool in_segment(const int32_t* __restrict__ cols, int64_t lo, int64_t hi, int32_t v,
+                                           unsigned& probes) {
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         const int32_t x = cols[mid];
@@ -331,24 +354,36 @@ int64_t expand_tile(int width) {
     return 128;
 }
 
-static size_t expand_smem(int64_t TD, int W, bool count_only) {
-    size_t b = sizeof(int64_t) * (TD + 1) * 2 + sizeof(int32_t) * (TD + 1) * W + (TD + 1);
-    b = (b + 15) & ~(size_t)15;
-    if (!count_only) b += sizeof(int32_t) * TD * (W + 1);
-    return b;
-}
+// shared-memory layout of one expand tile (TD merge steps => <= TD+1 rows)
+struct ExpandSmem {
+    size_t P, Beg, CB, Row, CL, Piv, Out, total;
+    __host__ __device__ ExpandSmem(int64_t TD, int W, int nb, bool count_only) {
+        const size_t R1 = (size_t)TD + 1;
+        P = 0;
+        Beg = P + 8 * R1;
+        CB = Beg + 8 * R1;
+        Row = CB + 8 * R1 * nb;
+        CL = Row + 4 * R1 * W;
+        Piv = CL + 4 * R1 * nb;
+        Out = (Piv + R1 + 15) & ~(size_t)15;
+        total = Out + (count_only ? 0 : 4 * (size_t)TD * (W + 1));
+    }
+};
 
 template <typename MaskT, bool kCountOnly>
 __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int64_t TD = a.TD;
     const int W = L.width;
-    int64_t* sP = reinterpret_cast<int64_t*>(smem);
-    int64_t* sBeg = sP + (TD + 1);
-    int32_t* sRow = reinterpret_cast<int32_t*>(sBeg + (TD + 1));
-    uint8_t* sPiv = reinterpret_cast<uint8_t*>(sRow + (TD + 1) * W);
-    size_t outoff = (sizeof(int64_t) * (TD + 1) * 2 + sizeof(int32_t) * (TD + 1) * W + (TD + 1) + 15) & ~(size_t)15;
-    int32_t* sOut = reinterpret_cast<int32_t*>(smem + outoff);
+    const int nb = L.nb;
+    const ExpandSmem lay(TD, W, nb, kCountOnly);
+    int64_t* sP = reinterpret_cast<int64_t*>(smem + lay.P);
+    int64_t* sBeg = reinterpret_cast<int64_t*>(smem + lay.Beg);
+    int64_t* sCB = reinterpret_cast<int64_t*>(smem + lay.CB);
+    int32_t* sRow = reinterpret_cast<int32_t*>(smem + lay.Row);
+    int32_t* sCL = reinterpret_cast<int32_t*>(smem + lay.CL);
+    uint8_t* sPiv = smem + lay.Piv;
+    int32_t* sOut = reinterpret_cast<int32_t*>(smem + lay.Out);
     __shared__ int sCount;
     __shared__ unsigned long long sBase;
     __shared__ unsigned long long sRed[kWarps][5];  // survivors, items, mask, probes, lists
@@ -376,6 +411,11 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
             const int32_t* src = a.F + ra0 * W;
             const int nq = nrows * W;
             for (int q = threadIdx.x; q < nq; q += kThreads) sRow[q] = src[q];
+            const int nc = nrows * nb;
+            for (int q = threadIdx.x; q < nc; q += kThreads) {
+                sCB[q] = a.cbeg[ra0 * nb + q];
+                sCL[q] = a.clen[ra0 * nb + q];
+            }
         }
         if (threadIdx.x == 0) sCount = 0;
         __syncthreads();
@@ -407,7 +447,8 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
                 for (int q = 0; q < L.nb && ok; ++q)
                     if (q != piv) {
                         ++st_lists;
-                        ok = in_list(a.off, a.cols, row[L.bpos[q]], v, st_probes);
+                        const int64_t cb = sCB[lr * nb + q];
+                        ok = in_segment(a.cols, cb, cb + sCL[lr * nb + q], v, st_probes);
                     }
             }
             if (kCountOnly) {
@@ -464,7 +505,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
 
 template <typename MaskT, bool kCountOnly>
 static void launch_expand_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
-    const size_t smem = expand_smem(a.TD, L.width, kCountOnly);
+    const size_t smem = ExpandSmem(a.TD, L.width, L.nb, kCountOnly).total;
     static bool configured = false;  // per template instance
     if (!configured) {
         GSM_CUDA(cudaFuncSetAttribute(k_expand<MaskT, kCountOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -33,8 +33,11 @@ int64_t launch_root_subset(const DevGraph& g, const void* cmask, int mask_bytes,
                            int64_t len, int32_t* roots, cudaStream_t s);
 
 // Per-row pivot choice and candidate range (the "Advance" source list).
+// Also writes, per row and per backward position q, the exact admissible segment of that
+// neighbour's list (cbeg/clen, R x nb): the pivot's is the candidate list, the others are
+// the membership lists the verify step binary-searches.
 void launch_plan_rows(const DevGraph& g, const int32_t* F, int64_t R, const LevelPlan& L, int64_t* rbeg,
-                      int64_t* rlen, uint8_t* rpiv, cudaStream_t s);
+                      int64_t* rlen, uint8_t* rpiv, int64_t* cbeg, int32_t* clen, cudaStream_t s);
 
 // Inclusive scan of rlen into P[1..R] (P[0] = 0); returns nothing (caller reads P[R]).
 size_t scan_temp_bytes(int64_t R);
@@ -50,6 +53,8 @@ struct ExpandArgs {
     const int64_t* P;      // R+1 work offsets
     const int64_t* rbeg;   // R pivot-range starts (index into cols)
     const uint8_t* rpiv;   // R pivot index into L.bpos
+    const int64_t* cbeg;   // R x nb admissible segment starts (index into cols)
+    const int32_t* clen;   // R x nb admissible segment lengths
     const int64_t* tile_ra;
     int64_t D0, D1, TD, ntiles;
     const int64_t* off;

@@ -75,7 +75,8 @@ struct Recorder {
 struct LevelBufs {
     DevBuf<int32_t> rows;  // frontier of this width (input rows of process(width))
     int64_t cap_rows = 0;  // row capacity reserved for this frontier (0 = unbounded roots)
-    DevBuf<int64_t> rbeg, rlen, P, tile_ra;
+    DevBuf<int64_t> rbeg, rlen, P, tile_ra, cbeg;
+    DevBuf<int32_t> clen;
     DevBuf<uint8_t> rpiv, scan_tmp;
     DevBuf<unsigned long long> out_count;
     unsigned long long* stats = nullptr;  // 5 counters for this width's expand launches
@@ -212,7 +213,7 @@ void Matcher::run() {
     const int nfront = count_mode_ ? std::max(0, k_ - 2) : k_ - 1;
     for (int w = 2; w <= k_; ++w) {
         const int64_t share = nfront > 0 ? budget_ / nfront : budget_;
-        const int64_t per_row = 4 * w + 8 * 3 + 1 + 1;  // rows + rbeg/rlen/P + piv + tile slack
+        const int64_t per_row = 4 * w + 8 * 3 + 1 + 1 + 12 * (w - 1);  // rows + rbeg/rlen/P + piv + segs
         lv_[w]->cap_rows = std::max<int64_t>(share / per_row, 1);
     }
 
@@ -237,8 +238,8 @@ void Matcher::run() {
             const LevelPlan& L = lplan_[w];
             // staged rows (entries + work offset + pivot start + pivot index), list entries read,
             // cmask bytes, membership lists (offset pair) and probes, survivor rows written
-            eb += lv_[w]->rows_in * (4.0 * w + 8 + 8 + 1) + 4.0 * st[0] + (double)mask_bytes_ * st[1] +
-                  16.0 * st[4] + 4.0 * st[2] + (L.count_only ? 0.0 : 4.0 * (w + 1) * st[3]);
+            eb += lv_[w]->rows_in * (4.0 * w + 8 + 8 + 1 + 12.0 * L.nb) + 4.0 * st[0] +
+                  (double)mask_bytes_ * st[1] + 4.0 * st[2] + (L.count_only ? 0.0 : 4.0 * (w + 1) * st[3]);
             res_->level_work[w] = st[0];
             res_->level_rows[w] = st[3];  // partial results with w+1 matched positions
         }
@@ -265,11 +266,13 @@ void Matcher::process(int w, const int32_t* F, int64_t R) {
     B.rbeg.ensure(R, s_);
     B.rlen.ensure(R, s_);
     B.rpiv.ensure(R, s_);
+    B.cbeg.ensure((size_t)R * L.nb, s_);
+    B.clen.ensure((size_t)R * L.nb, s_);
     B.P.ensure(R + 1, s_);
     const size_t tb = scan_temp_bytes(R);
     B.scan_tmp.ensure(tb, s_);
-    rec_.run(GSM_K_PLAN, 1, [&] { launch_plan_rows(g_, F, R, L, B.rbeg.p, B.rlen.p, B.rpiv.p, s_); });
-    res_->prof[GSM_K_PLAN].alg_bytes += (double)R * (4.0 * w + 16.0 * L.nb + 8 + 8 + 1);
+    rec_.run(GSM_K_PLAN, 1, [&] { launch_plan_rows(g_, F, R, L, B.rbeg.p, B.rlen.p, B.rpiv.p, B.cbeg.p, B.clen.p, s_); });
+    res_->prof[GSM_K_PLAN].alg_bytes += (double)R * (4.0 * w + 16.0 * L.nb + 12.0 * L.nb + 8 + 8 + 1);
     rec_.run(GSM_K_SCAN, 1, [&] { launch_scan(B.rlen.p, R, B.P.p, B.scan_tmp.p, tb, s_); });
     res_->prof[GSM_K_SCAN].alg_bytes += (double)R * 16.0;
     const int64_t S = read_scalar(B.P.p + R, s_);
@@ -297,6 +300,8 @@ void Matcher::process(int w, const int32_t* F, int64_t R) {
     a.P = B.P.p;
     a.rbeg = B.rbeg.p;
     a.rpiv = B.rpiv.p;
+    a.cbeg = B.cbeg.p;
+    a.clen = B.clen.p;
     a.tile_ra = B.tile_ra.p;
     a.TD = TD;
     a.off = g_.off;

@@ -230,6 +230,8 @@ def run_ours(args, world, rank, local, dist):
     if graph_bytes <= 126e6:
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    per_query = {}
+
     def step(flags, G_=None):
         G_ = G_ or G
         tot_all = tot_unique = launches = 0
@@ -241,6 +243,11 @@ def run_ours(args, world, rank, local, dist):
             tot_unique += r.count_unique
             launches += r.kernel_launches
             profs.append(r.prof)
+            per_query[q.name] = {"count": r.count, "unique": r.count_unique, "automorphisms": r.automorphisms,
+                                 "order": r.order, "candidates": r.candidates, "level_work": r.level_work,
+                                 "level_rows": r.level_rows, "chunks": r.num_chunks,
+                                 "ms": {k: round(v, 3) for k, v in r.ms.items()},
+                                 "kernel_ms": {k: round(v["ms"], 3) for k, v in r.prof.items()}}
         return tot_all, tot_unique, launches, profs
 
     def barrier():
@@ -341,7 +348,7 @@ def run_ours(args, world, rank, local, dist):
            "config": config_of(w, g),
            "counts_per_step": {"all": c_all, "unique": c_uni},
            "unique_per_s": c_uni / (ms / 1000.0),
-           "query_ms": ms, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
+           "query_ms": ms, "per_query_rank0": per_query, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(g, w, args.cpu_seconds)

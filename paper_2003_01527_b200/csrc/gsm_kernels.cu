@@ -354,44 +354,42 @@ int64_t expand_tile(int width) {
     return 128;
 }
 
-// Verify-list staging: per tile and per (row, check list), the part of the
-// check segment that can contain this tile's candidates of that row lies
-// between the row's first and last candidate (pivot segments are sorted), so
-// it is narrowed by two binary searches and, when short, copied coalesced into
-// a shared-memory pool; every candidate's membership test then runs as a
-// shared-memory binary search instead of a chain of dependent global loads.
-constexpr int kPool = 3072;      // int32 elements staged per tile (12 KB)
-constexpr int kMaxStage = 2048;  // longest sub-segment staged
-
-// shared-memory layout of one expand tile (TD merge steps => <= TD+1 rows)
+// shared-memory layout of one expand tile (TD merge steps => <= TD+1 rows, <= TD items)
 struct ExpandSmem {
-    size_t P, Beg, CB, Row, CL, PO, Wn, Piv, Pool, Out, total;
+    size_t P, Beg, CB, Row, CL, RowOf, Piv, Out, total;
     __host__ __device__ ExpandSmem(int64_t TD, int W, int nb, bool count_only) {
         const size_t R1 = (size_t)TD + 1;
-        P = 0;                         // int64 [R1+1]  work offsets of the tile's rows
-        Beg = P + 8 * (R1 + 1);        // int64 [R1]    pivot segment start
-        CB = Beg + 8 * R1;             // int64 [R1*nb] check segment start (narrowed per tile)
-        Row = CB + 8 * R1 * nb;        // int32 [R1*W]  row entries
-        CL = Row + 4 * R1 * W;         // int32 [R1*nb] check segment length
-        PO = CL + 4 * R1 * nb;         // int32 [R1*nb] pool offset (-1 = not staged)
-        Wn = PO + 4 * R1 * nb;         // int32 [R1*nb] staging request
-        Pool = Wn + 4 * R1 * nb;       // int32 [kPool]
-        Piv = Pool + 4 * (size_t)kPool;  // uint8 [R1]
+        P = 0;                     // int64 [R1+1]  work offsets of the tile's rows
+        Beg = P + 8 * (R1 + 1);    // int64 [R1]    pivot segment start
+        CB = Beg + 8 * R1;         // int64 [R1*nb] membership segment start
+        Row = CB + 8 * R1 * nb;    // int32 [R1*W]  row entries
+        CL = Row + 4 * R1 * W;     // int32 [R1*nb] membership segment length
+        RowOf = CL + 4 * R1 * nb;  // int32 [TD]    item -> local row (scatter + max-scan)
+        Piv = RowOf + 4 * (size_t)TD;  // uint8 [R1]
         Out = (Piv + R1 + 15) & ~(size_t)15;
         total = Out + (count_only ? 0 : 4 * (size_t)TD * (W + 1));
     }
 };
 
-__device__ __forceinline__ bool in_smem(const int32_t* __restrict__ a, int len, int32_t v) {
-    int lo = 0, hi = len;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const int32_t x = a[mid];
-        if (x == v) return true;
-        if (x < v) lo = mid + 1; else hi = mid;
+// membership of v in the sorted segment a[0, len): branch-free lower bound
+// (fixed trip count, predicated steps) followed by one equality test
+__device__ __forceinline__ bool in_sorted(const int32_t* __restrict__ a, int len, int32_t v, unsigned& probes) {
+    if (len <= 0) return false;
+    const int32_t* base = a;
+    int n = len;
+    while (n > 1) {
+        const int half = n >> 1;
+        base = (base[half - 1] < v) ? base + half : base;
+        n -= half;
+        ++probes;
     }
-    return false;
+    ++probes;
+    return *base == v;
 }
+
+struct MaxOp {
+    __device__ __forceinline__ int operator()(int x, int y) const { return x > y ? x : y; }
+};
 
 template <typename MaskT, bool kCountOnly>
 __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) {
@@ -405,23 +403,22 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
     int64_t* sCB = reinterpret_cast<int64_t*>(smem + lay.CB);
     int32_t* sRow = reinterpret_cast<int32_t*>(smem + lay.Row);
     int32_t* sCL = reinterpret_cast<int32_t*>(smem + lay.CL);
-    int32_t* sPO = reinterpret_cast<int32_t*>(smem + lay.PO);
-    int32_t* sWn = reinterpret_cast<int32_t*>(smem + lay.Wn);
-    int32_t* sPool = reinterpret_cast<int32_t*>(smem + lay.Pool);
+    int32_t* sRowOf = reinterpret_cast<int32_t*>(smem + lay.RowOf);
     uint8_t* sPiv = smem + lay.Piv;
     int32_t* sOut = reinterpret_cast<int32_t*>(smem + lay.Out);
     using BlockScan = cub::BlockScan<int, kThreads>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
     __shared__ int sCount;
     __shared__ unsigned long long sBase;
-    __shared__ unsigned long long sRed[kWarps][5];  // survivors, items, mask, probes, staged
+    __shared__ unsigned long long sRed[kWarps][5];  // survivors, items, mask, probes, lists
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
     const int32_t* __restrict__ cols = a.cols;
+    const int per_thread = (int)((TD + kThreads - 1) / kThreads);
     unsigned long long cnt = 0;
-    unsigned st_items = 0, st_mask = 0, st_probes = 0, st_staged = 0;
+    unsigned st_items = 0, st_mask = 0, st_probes = 0, st_lists = 0;
 
     for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         const int64_t d0 = a.D0 + t * TD;
@@ -429,11 +426,12 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
         const int64_t ra0 = a.tile_ra[t], ra1 = a.tile_ra[t + 1];
         const int64_t ib0 = d0 - ra0, ib1 = d1 - ra1;
         if (ib1 <= ib0) continue;  // block-uniform
+        const int nitems = (int)(ib1 - ib0);
         const int64_t rlast = min(ra1, a.R - 1);
         const int nrows = (int)(rlast - ra0 + 1);
-        const int nc = nrows * nb;
         __syncthreads();  // previous tile finished with shared memory
-        // ---- stage the tile's rows
+        // ---- stage the tile's rows; mark where each non-empty row starts
+        for (int i = threadIdx.x; i < nitems; i += kThreads) sRowOf[i] = 0;
         for (int lr = threadIdx.x; lr <= nrows; lr += kThreads) sP[lr] = a.P[ra0 + lr];
         for (int lr = threadIdx.x; lr < nrows; lr += kThreads) {
             sBeg[lr] = a.rbeg[ra0 + lr];
@@ -443,6 +441,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
             const int32_t* src = a.F + ra0 * W;
             const int nq = nrows * W;
             for (int q = threadIdx.x; q < nq; q += kThreads) sRow[q] = src[q];
+            const int nc = nrows * nb;
             for (int q = threadIdx.x; q < nc; q += kThreads) {
                 sCB[q] = a.cbeg[ra0 * nb + q];
                 sCL[q] = a.clen[ra0 * nb + q];
@@ -450,69 +449,36 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
         }
         if (threadIdx.x == 0) sCount = 0;
         __syncthreads();
-        // ---- narrow every check segment to this tile's candidate range; request staging
-        for (int e = threadIdx.x; e < nc; e += kThreads) {
-            const int lr = e / nb, q = e - lr * nb;
-            int want = 0;
-            if (q != sPiv[lr]) {
-                const int64_t x0 = max(ib0, sP[lr]), x1 = min(ib1, sP[lr + 1]);
-                int64_t s = sCB[e], u = s + sCL[e];
-                if (x1 - x0 >= 2) {
-                    if (u - s > 8) {
-                        const int32_t vmin = cols[sBeg[lr] + (x0 - sP[lr])];
-                        const int32_t vmax = cols[sBeg[lr] + (x1 - 1 - sP[lr])];
-                        s = lower_bound_cols(cols, s, u, vmin);
-                        u = lower_bound_cols(cols, s, u, (int64_t)vmax + 1);
-                        sCB[e] = s;
-                        sCL[e] = (int32_t)(u - s);
-                    }
-                    want = (u - s <= kMaxStage) ? (int)(u - s) : 0;
-                }
-            }
-            sWn[e] = want;
+        for (int lr = threadIdx.x; lr < nrows; lr += kThreads) {
+            const int64_t s = max(sP[lr], ib0), e = min(sP[lr + 1], ib1);
+            if (e > s) sRowOf[s - ib0] = lr;  // rows with items in this tile start at distinct slots
         }
         __syncthreads();
-        // ---- pool allocation: exclusive scan of the requests (contiguous chunk per thread)
+        // ---- item -> row: inclusive max-scan (each thread owns a contiguous run of slots)
         {
-            const int per = (nc + kThreads - 1) / kThreads;
-            const int e0 = min(nc, (int)threadIdx.x * per), e1 = min(nc, e0 + per);
-            int mine = 0;
-            for (int e = e0; e < e1; ++e) mine += sWn[e];
-            int off;
-            BlockScan(scan_tmp).ExclusiveSum(mine, off);
-            for (int e = e0; e < e1; ++e) {
-                const int wn = sWn[e];
-                sPO[e] = (wn > 0 && off + wn <= kPool) ? off : -1;
-                off += wn;
+            const int i0 = min(nitems, (int)threadIdx.x * per_thread), i1 = min(nitems, i0 + per_thread);
+            int mx = 0;
+            for (int i = i0; i < i1; ++i) mx = max(mx, sRowOf[i]);
+            int prefix;
+            BlockScan(scan_tmp).ExclusiveScan(mx, prefix, MaxOp());
+            if (threadIdx.x == 0) prefix = 0;
+            for (int i = i0; i < i1; ++i) {
+                prefix = max(prefix, sRowOf[i]);
+                sRowOf[i] = prefix;
             }
-        }
-        __syncthreads();
-        // ---- coalesced copy of the staged sub-segments (warp per segment)
-        for (int e = warp; e < nc; e += kWarps) {
-            const int po = sPO[e];
-            if (po < 0) continue;
-            const int len = sCL[e];
-            const int32_t* src = cols + sCB[e];
-            for (int i = lane; i < len; i += 32) sPool[po + i] = src[i];
-            if (lane == 0) st_staged += len;
         }
         __syncthreads();
 
-        // ---- candidates
-        for (int64_t base = ib0; base < ib1; base += kThreads) {
-            const int64_t x = base + threadIdx.x;
+        // ---- candidates (consecutive threads read consecutive list entries)
+        for (int base = 0; base < nitems; base += kThreads) {
+            const int xi = base + threadIdx.x;
             bool ok = false;
             int lr = 0;
             int32_t v = 0;
-            if (x < ib1) {
+            if (xi < nitems) {
                 ++st_items;
-                int lo = 0, hi = nrows;  // largest lr with sP[lr] <= x
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (sP[mid] <= x) lo = mid + 1; else hi = mid;
-                }
-                lr = lo - 1;
-                v = cols[sBeg[lr] + (x - sP[lr])];
+                lr = sRowOf[xi];
+                v = cols[sBeg[lr] + ((ib0 + xi) - sP[lr])];
                 const int32_t* row = sRow + lr * W;
                 ok = true;
                 for (int q = 0; q < L.nlo && ok; ++q) ok = v > row[L.lo[q]];
@@ -525,14 +491,9 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
                 const int piv = sPiv[lr];
                 for (int q = 0; q < nb && ok; ++q) {
                     if (q == piv) continue;
+                    ++st_lists;
                     const int e = lr * nb + q;
-                    const int po = sPO[e];
-                    if (po >= 0) {
-                        ok = in_smem(sPool + po, sCL[e], v);
-                    } else {
-                        const int64_t cb = sCB[e];
-                        ok = in_segment(cols, cb, cb + sCL[e], v, st_probes);
-                    }
+                    ok = in_sorted(cols + sCB[e], sCL[e], v, st_probes);
                 }
             }
             if (kCountOnly) {
@@ -563,7 +524,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
         }
     }
     // block reduction of the counters
-    unsigned long long v5[5] = {cnt, st_items, st_mask, st_probes, st_staged};
+    unsigned long long v5[5] = {cnt, st_items, st_mask, st_probes, st_lists};
 #pragma unroll
     for (int c = 0; c < 5; ++c)
         for (int o = 16; o; o >>= 1) v5[c] += __shfl_xor_sync(0xffffffffu, v5[c], o);
@@ -579,9 +540,9 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
                 if (kCountOnly) atomicAdd(a.out_count, s);
                 atomicAdd(&a.stats[3], s);  // survivors
             } else if (threadIdx.x < 4) {
-                atomicAdd(&a.stats[threadIdx.x - 1], s);  // items, mask_checked, global probes
+                atomicAdd(&a.stats[threadIdx.x - 1], s);  // items, mask_checked, probes
             } else {
-                atomicAdd(&a.stats[4], s);  // check-list elements staged in shared memory
+                atomicAdd(&a.stats[4], s);  // membership lists searched
             }
         }
     }

@@ -62,7 +62,7 @@ struct ExpandArgs {
     const void* cmask;
     int32_t* out;          // survivors (width+1 ints each), unless count_only
     unsigned long long* out_count;  // survivors (atomic)
-    unsigned long long* stats;      // [items, mask_checked, global probes, survivors, staged elements]
+    unsigned long long* stats;      // [items, mask_checked, probes, survivors, lists]
 };
 
 // Tile size (merge steps per CTA) for a given input width.

@@ -236,12 +236,10 @@ void Matcher::run() {
         for (int w = 1; w < k_; ++w) {
             const unsigned long long* st = hs.data() + 5 * w;
             const LevelPlan& L = lplan_[w];
-            // staged rows (entries, work offsets, pivot start + index, check segments), list
-            // entries read, cmask bytes, global binary-search probes, check-list elements
-            // staged in shared memory, survivor rows written
+            // staged rows (entries, work offsets, pivot start + index, membership segments),
+            // list entries read, cmask bytes, binary-search probes, survivor rows written
             eb += lv_[w]->rows_in * (4.0 * w + 8 + 8 + 1 + 12.0 * L.nb) + 4.0 * st[0] +
-                  (double)mask_bytes_ * st[1] + 4.0 * st[2] + 4.0 * st[4] +
-                  (L.count_only ? 0.0 : 4.0 * (w + 1) * st[3]);
+                  (double)mask_bytes_ * st[1] + 4.0 * st[2] + (L.count_only ? 0.0 : 4.0 * (w + 1) * st[3]);
             res_->level_work[w] = st[0];
             res_->level_rows[w] = st[3];  // partial results with w+1 matched positions
         }

@@ -21,6 +21,11 @@ struct DevGraph {
     int32_t* cols = nullptr;      // nnz, ascending per list (new ids)
     int32_t* up = nullptr;        // n: neighbours with smaller new id; N+(v) = cols[off[v]+up[v], off[v+1])
     uint32_t* labels = nullptr;   // n (new ids) or nullptr
+    // label-grouped lists (labeled graphs whose label and id bits fit 31 bits): list of v
+    // re-sorted by (label(w), w), stored as keys label(w) << idbits | w, same offsets
+    int32_t* lkeys = nullptr;
+    int32_t idbits = 0;
+    uint32_t max_label = 0;
     int32_t* new2old = nullptr;   // n
     int32_t* old2new = nullptr;   // n
     int32_t max_degree = 0;

@@ -139,6 +139,27 @@ __global__ void k_up(const int64_t* __restrict__ off, const int32_t* __restrict_
     }
 }
 
+__global__ void k_max_label(const uint32_t* __restrict__ labels, int64_t n, unsigned* out) {
+    unsigned m = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, labels[v]);
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// warp per vertex p of the relabelled CSR: key (p, label(w) << idbits | w)
+__global__ void k_label_edge_keys(const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                                  const uint32_t* __restrict__ labels, int64_t n, int idbits, uint64_t* ekeys) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = warp; p < n; p += nwarps)
+        for (int64_t i = off[p] + lane; i < off[p + 1]; i += 32) {
+            const int32_t w = cols[i];
+            ekeys[i] = ((uint64_t)p << 32) | (((uint64_t)labels[w] << idbits) | (uint32_t)w);
+        }
+}
+
 __global__ void k_permute_labels(const uint32_t* __restrict__ labels, const int32_t* __restrict__ new2old, int64_t n,
                                  uint32_t* out) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
@@ -169,6 +190,7 @@ static void free_graph(gsm_graph* h) {
     cudaFree(g.cols);
     cudaFree(g.up);
     cudaFree(g.labels);
+    cudaFree(g.lkeys);
     cudaFree(g.new2old);
     cudaFree(g.old2new);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -318,6 +340,36 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         k_permute_labels<<<grid_for(n), 256, 0, s>>>(d_lab, g.new2old, n, g.labels);
         GSM_LAUNCH("k_permute_labels");
         h->labeled = true;
+        // label-grouped lists: each list re-sorted by (label, id) as packed 31-bit keys,
+        // so a labeled query's admissible candidates form one contiguous segment
+        DevBuf<unsigned> maxl;
+        maxl.ensure(1, s);
+        GSM_CUDA(cudaMemsetAsync(maxl.p, 0, sizeof(unsigned), s));
+        k_max_label<<<grid_for(n), 256, 0, s>>>(g.labels, n, maxl.p);
+        GSM_LAUNCH("k_max_label");
+        unsigned hmax = 0;
+        GSM_CUDA(cudaMemcpyAsync(&hmax, maxl.p, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        const int idbits = bits_for((uint64_t)(n > 1 ? n - 1 : 1));
+        const int lbits = hmax ? bits_for((uint64_t)hmax) : 0;
+        g.max_label = hmax;
+        if (nnz > 0 && idbits + lbits <= 31) {
+            g.idbits = idbits;
+            GSM_CUDA(cudaMalloc(&g.lkeys, sizeof(int32_t) * nnz));
+            DevBuf<uint64_t> ekeys, esorted;
+            ekeys.ensure(nnz, s);
+            esorted.ensure(nnz, s);
+            k_label_edge_keys<<<grid_for(n * 32), 256, 0, s>>>(g.off, g.cols, g.labels, n, idbits, ekeys.p);
+            GSM_LAUNCH("k_label_edge_keys");
+            const int end_bit = 32 + bits_for((uint64_t)n);
+            size_t tmp_bytes = 0;
+            GSM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, ekeys.p, esorted.p, nnz, 0, end_bit, s));
+            DevBuf<uint8_t> tmp;
+            tmp.ensure(tmp_bytes, s);
+            GSM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, ekeys.p, esorted.p, nnz, 0, end_bit, s));
+            k_extract_cols<<<grid_for(nnz), 256, 0, s>>>(esorted.p, nnz, g.lkeys);
+            GSM_LAUNCH("k_extract_cols(lkeys)");
+        }
     }
     GSM_CUDA(cudaStreamSynchronize(s));
     *out = h.release();

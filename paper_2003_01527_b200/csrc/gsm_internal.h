@@ -64,6 +64,11 @@ struct LevelPlan {
     int32_t ninj;        // positions needing an explicit injectivity compare
     int32_t inj[kMaxK];
     int32_t count_only;  // last level in COUNT mode: count survivors, write nothing
+    // label-grouped lists (set by the driver when the graph has them and Q is labeled):
+    // candidates are keys key_base | id in the (label, id)-sorted lists; idmask decodes
+    int32_t keyed;
+    int32_t key_base;
+    int32_t idmask;
 };
 
 LevelPlan make_level_plan(const QueryPlan& p, int i, bool count_only);

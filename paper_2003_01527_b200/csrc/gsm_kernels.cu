@@ -11,6 +11,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gsm_kernels.h"
 
@@ -248,26 +249,45 @@ __global__ void __launch_bounds__(kThreads) k_plan_rows(const int32_t* __restric
         for (int q = 0; q < L.nlo; ++q) lov = max(lov, (int64_t)row[L.lo[q]]);
         for (int q = 0; q < L.nhi; ++q) hiv = min(hiv, (int64_t)row[L.hi[q]]);
         const bool empty = lov + 1 >= hiv;
-        // pivot = shortest estimated segment (up-split only, no search yet)
-        int64_t blen = INT64_MAX;
-        int bq = 0;
-        for (int q = 0; q < nb; ++q) {
-            int64_t s0, t0;
-            admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, false, s0, t0);
-            if (t0 - s0 < blen) { blen = t0 - s0; bq = q; }
-        }
-        // exact segments: the pivot's (its length is the work of this row) and the
-        // membership lists of the other backward neighbours (searched per candidate)
         int64_t ps = 0, pt = 0;
-        for (int q = 0; q < nb; ++q) {
-            int64_t s0, t0;
-            const bool pivot = q == bq;
-            admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, !empty && (pivot ? blen > 8 : true),
-                               s0, t0);
-            if (empty) t0 = s0;
-            cbeg[r * nb + q] = s0;
-            clen[r * nb + q] = (int32_t)(t0 - s0);
-            if (pivot) { ps = s0; pt = t0; }
+        int bq = 0;
+        if (L.keyed) {
+            // (label, id)-sorted lists: the admissible keys [base|lov+1, base+hiv) are one segment
+            int64_t blen = INT64_MAX;
+            const int64_t klo = (int64_t)L.key_base + lov + 1, khi = (int64_t)L.key_base + hiv;
+            for (int q = 0; q < nb; ++q) {
+                const int32_t a = row[L.bpos[q]];
+                int64_t s0 = off[a], t0 = off[a + 1];
+                if (!empty) {
+                    s0 = lower_bound_cols(cols, s0, t0, klo);
+                    t0 = lower_bound_cols(cols, s0, t0, khi);
+                } else {
+                    t0 = s0;
+                }
+                cbeg[r * nb + q] = s0;
+                clen[r * nb + q] = (int32_t)(t0 - s0);
+                if (t0 - s0 < blen) { blen = t0 - s0; bq = q; ps = s0; pt = t0; }
+            }
+        } else {
+            // pivot = shortest estimated segment (up-split only, no search yet)
+            int64_t blen = INT64_MAX;
+            for (int q = 0; q < nb; ++q) {
+                int64_t s0, t0;
+                admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, false, s0, t0);
+                if (t0 - s0 < blen) { blen = t0 - s0; bq = q; }
+            }
+            // exact segments: the pivot's (its length is the work of this row) and the
+            // membership lists of the other backward neighbours (searched per candidate)
+            for (int q = 0; q < nb; ++q) {
+                int64_t s0, t0;
+                const bool pivot = q == bq;
+                admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, !empty && (pivot ? blen > 8 : true),
+                                   s0, t0);
+                if (empty) t0 = s0;
+                cbeg[r * nb + q] = s0;
+                clen[r * nb + q] = (int32_t)(t0 - s0);
+                if (pivot) { ps = s0; pt = t0; }
+            }
         }
         rbeg[r] = ps;
         rlen[r] = pt - ps;
@@ -277,7 +297,8 @@ __global__ void __launch_bounds__(kThreads) k_plan_rows(const int32_t* __restric
 
 void launch_plan_rows(const DevGraph& g, const int32_t* F, int64_t R, const LevelPlan& L, int64_t* rbeg,
                       int64_t* rlen, uint8_t* rpiv, int64_t* cbeg, int32_t* clen, cudaStream_t s) {
-    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, g.cols, g.up, g.n, rbeg, rlen, rpiv, cbeg, clen);
+    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, L.keyed ? g.lkeys : g.cols, g.up, g.n, rbeg, rlen,
+                                                 rpiv, cbeg, clen);
     GSM_LAUNCH("k_plan_rows");
 }
 
@@ -349,8 +370,15 @@ __device__ __forceinline__ bool in_segment(const int32_t* __restrict__ cols, int
 }
 
 int64_t expand_tile(int width) {
-    if (width <= 4) return 512;
-    if (width <= 12) return 256;
+    static int td = -1;
+    if (td < 0) {
+        const char* v = getenv("GSM_EXPAND_TD");
+        td = (v && *v) ? atoi(v) : 512;
+        if (td < 128) td = 128;
+        if (td > 2048) td = 2048;
+    }
+    if (width <= 4) return td;
+    if (width <= 12) return std::min(td, 256);
     return 128;
 }
 
@@ -391,7 +419,7 @@ struct MaxOp {
     __device__ __forceinline__ int operator()(int x, int y) const { return x > y ? x : y; }
 };
 
-template <typename MaskT, bool kCountOnly>
+template <typename MaskT, bool kCountOnly, int U>
 __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int64_t TD = a.TD;
@@ -469,46 +497,95 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
         }
         __syncthreads();
 
-        // ---- candidates (consecutive threads read consecutive list entries)
-        for (int base = 0; base < nitems; base += kThreads) {
-            const int xi = base + threadIdx.x;
-            bool ok = false;
-            int lr = 0;
-            int32_t v = 0;
-            if (xi < nitems) {
-                ++st_items;
-                lr = sRowOf[xi];
-                v = cols[sBeg[lr] + ((ib0 + xi) - sP[lr])];
-                const int32_t* row = sRow + lr * W;
-                ok = true;
-                for (int q = 0; q < L.nlo && ok; ++q) ok = v > row[L.lo[q]];
-                for (int q = 0; q < L.nhi && ok; ++q) ok = v < row[L.hi[q]];
-                if (ok && L.check_mask) {
-                    ++st_mask;
-                    ok = (cmask[v] >> L.qv) & 1u;
-                }
-                for (int q = 0; q < L.ninj && ok; ++q) ok = v != row[L.inj[q]];
-                const int piv = sPiv[lr];
-                for (int q = 0; q < nb && ok; ++q) {
-                    if (q == piv) continue;
-                    ++st_lists;
-                    const int e = lr * nb + q;
-                    ok = in_sorted(cols + sCB[e], sCL[e], v, st_probes);
+        // ---- candidates: each thread carries U items at once (items base + j*kThreads + tid,
+        //      consecutive threads read consecutive list entries) and advances their
+        //      membership searches in lockstep, so U independent loads are in flight per
+        //      thread instead of one dependent chain
+        for (int base = 0; base < nitems; base += kThreads * U) {
+            int lr[U];
+            int32_t v[U];
+            bool ok[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int xi = base + j * kThreads + threadIdx.x;
+                ok[j] = xi < nitems;
+                lr[j] = 0;
+                v[j] = 0;
+                if (ok[j]) {
+                    ++st_items;
+                    lr[j] = sRowOf[xi];
+                    v[j] = cols[sBeg[lr[j]] + ((ib0 + xi) - sP[lr[j]])] & L.idmask;
                 }
             }
-            if (kCountOnly) {
-                cnt += ok ? 1u : 0u;
-            } else {
-                const unsigned ball = __ballot_sync(0xffffffffu, ok);
-                int wbase = 0;
-                if (lane == 0 && ball) wbase = atomicAdd(&sCount, __popc(ball));
-                wbase = __shfl_sync(0xffffffffu, wbase, 0);
-                if (ok) {
-                    const int pos = wbase + __popc(ball & ((1u << lane) - 1u));
-                    int32_t* o = sOut + (int64_t)pos * (W + 1);
-                    const int32_t* row = sRow + lr * W;
-                    for (int c = 0; c < W; ++c) o[c] = row[c];
-                    o[W] = v;
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (!ok[j]) continue;
+                const int32_t* row = sRow + lr[j] * W;
+                for (int q = 0; q < L.nlo && ok[j]; ++q) ok[j] = v[j] > row[L.lo[q]];
+                for (int q = 0; q < L.nhi && ok[j]; ++q) ok[j] = v[j] < row[L.hi[q]];
+                for (int q = 0; q < L.ninj && ok[j]; ++q) ok[j] = v[j] != row[L.inj[q]];
+            }
+            if (L.check_mask) {
+                uint32_t m[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j)
+                    if (ok[j]) { ++st_mask; m[j] = cmask[v[j]]; }
+#pragma unroll
+                for (int j = 0; j < U; ++j)
+                    if (ok[j]) ok[j] = (m[j] >> L.qv) & 1u;
+            }
+            for (int q = 0; q < nb; ++q) {
+                const int32_t* pb[U];
+                int pn[U];
+                bool act[U];
+                bool more = false;
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    act[j] = ok[j] && q != sPiv[lr[j]];
+                    pn[j] = 0;
+                    pb[j] = cols;
+                    if (act[j]) {
+                        ++st_lists;
+                        const int e = lr[j] * nb + q;
+                        pb[j] = cols + sCB[e];
+                        pn[j] = sCL[e];
+                        if (pn[j] <= 0) { ok[j] = false; act[j] = false; }
+                        more |= pn[j] > 1;
+                    }
+                }
+                while (more) {  // branch-free lower bounds, advanced together
+                    more = false;
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        if (pn[j] > 1) {
+                            const int half = pn[j] >> 1;
+                            pb[j] = (pb[j][half - 1] < (L.key_base | v[j])) ? pb[j] + half : pb[j];
+                            pn[j] -= half;
+                            ++st_probes;
+                            more |= pn[j] > 1;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < U; ++j)
+                    if (act[j]) { ++st_probes; ok[j] = (*pb[j] == (L.key_base | v[j])); }
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                if (kCountOnly) {
+                    cnt += ok[j] ? 1u : 0u;
+                } else {
+                    const unsigned ball = __ballot_sync(0xffffffffu, ok[j]);
+                    int wbase = 0;
+                    if (lane == 0 && ball) wbase = atomicAdd(&sCount, __popc(ball));
+                    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+                    if (ok[j]) {
+                        const int pos = wbase + __popc(ball & ((1u << lane) - 1u));
+                        int32_t* o = sOut + (int64_t)pos * (W + 1);
+                        const int32_t* row = sRow + lr[j] * W;
+                        for (int c = 0; c < W; ++c) o[c] = row[c];
+                        o[W] = v[j];
+                    }
                 }
             }
         }
@@ -548,22 +625,46 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
     }
 }
 
-template <typename MaskT, bool kCountOnly>
-static void launch_expand_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
+// items carried per thread (memory-level parallelism of the membership searches)
+static int expand_ilp() {
+    static int u = -1;
+    if (u < 0) {
+        u = env_int("GSM_EXPAND_ILP", 4);
+        if (u != 1 && u != 2 && u != 4) u = 4;
+    }
+    return u;
+}
+
+template <typename MaskT, bool kCountOnly, int U>
+static void launch_expand_u(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
     const size_t smem = ExpandSmem(a.TD, L.width, L.nb, kCountOnly).total;
     static bool configured = false;  // per template instance
     if (!configured) {
-        GSM_CUDA(cudaFuncSetAttribute(k_expand<MaskT, kCountOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GSM_CUDA(cudaFuncSetAttribute(k_expand<MaskT, kCountOnly, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       200 * 1024));
         configured = true;
     }
     int dev = 0, sms = 148, per_sm = 1;
     GSM_CUDA(cudaGetDevice(&dev));
     GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand<MaskT, kCountOnly>, kThreads, smem));
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_expand<MaskT, kCountOnly, U>, kThreads, smem));
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(a.ntiles, (int64_t)sms * std::max(per_sm, 1)));
-    k_expand<MaskT, kCountOnly><<<(unsigned)grid, kThreads, smem, s>>>(a, L);
+    k_expand<MaskT, kCountOnly, U><<<(unsigned)grid, kThreads, smem, s>>>(a, L);
     GSM_LAUNCH("k_expand");
+}
+
+template <typename MaskT, bool kCountOnly>
+static void launch_expand_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
+    switch (expand_ilp()) {
+        case 1: launch_expand_u<MaskT, kCountOnly, 1>(a, L, s); break;
+        case 2: launch_expand_u<MaskT, kCountOnly, 2>(a, L, s); break;
+        default: launch_expand_u<MaskT, kCountOnly, 4>(a, L, s); break;
+    }
 }
 
 void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cudaStream_t s) {

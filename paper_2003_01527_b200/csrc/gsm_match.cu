@@ -169,7 +169,16 @@ void Matcher::run() {
     lv_.resize(k_ + 1);
     for (int w = 0; w <= k_; ++w) lv_[w].reset(new LevelBufs());
     lplan_.resize(k_);
-    for (int i = 1; i < k_; ++i) lplan_[i] = make_level_plan(plan_, i, count_mode_ && i == k_ - 1);
+    for (int i = 1; i < k_; ++i) {
+        LevelPlan& L = lplan_[i];
+        L = make_level_plan(plan_, i, count_mode_ && i == k_ - 1);
+        if (plan_.use_labels && g_.lkeys && plan_.qlabel[L.qv] <= g_.max_label) {
+            L.keyed = 1;
+            L.key_base = (int32_t)(plan_.qlabel[L.qv] << g_.idbits);
+            L.idmask = (int32_t)((1u << g_.idbits) - 1u);
+            L.check_mask = plan_.qdeg[L.qv] > L.nb ? 1 : 0;  // the label is implied by the key range
+        }
+    }
 
     // ---- roots = C(π[0]) (level-0 frontier)
     int64_t R0 = 0;
@@ -305,7 +314,7 @@ void Matcher::process(int w, const int32_t* F, int64_t R) {
     a.tile_ra = B.tile_ra.p;
     a.TD = TD;
     a.off = g_.off;
-    a.cols = g_.cols;
+    a.cols = L.keyed ? g_.lkeys : g_.cols;
     a.cmask = cmask_.p;
     a.stats = B.stats;
     B.rows_in += (double)R;

@@ -213,6 +213,9 @@ LevelPlan make_level_plan(const QueryPlan& p, int i, bool count_only) {
     for (int j = 0; j < i; ++j)
         if (!((covered >> j) & 1u)) L.inj[L.ninj++] = j;
     L.check_mask = (p.use_labels || p.qdeg[L.qv] > L.nb) ? 1 : 0;
+    L.keyed = 0;
+    L.key_base = 0;
+    L.idmask = -1;
     return L;
 }
 

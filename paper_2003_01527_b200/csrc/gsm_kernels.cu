@@ -634,8 +634,8 @@ static int env_int(const char* name, int dflt) {
 static int expand_ilp() {
     static int u = -1;
     if (u < 0) {
-        u = env_int("GSM_EXPAND_ILP", 4);
-        if (u != 1 && u != 2 && u != 4) u = 4;
+        u = env_int("GSM_EXPAND_ILP", 1);  // measured: 1 beats 2/4 (issue-bound, not latency-bound)
+        if (u != 1 && u != 2 && u != 4) u = 1;
     }
     return u;
 }
@@ -663,7 +663,8 @@ static void launch_expand_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_
     switch (expand_ilp()) {
         case 1: launch_expand_u<MaskT, kCountOnly, 1>(a, L, s); break;
         case 2: launch_expand_u<MaskT, kCountOnly, 2>(a, L, s); break;
-        default: launch_expand_u<MaskT, kCountOnly, 4>(a, L, s); break;
+        case 4: launch_expand_u<MaskT, kCountOnly, 4>(a, L, s); break;
+        default: launch_expand_u<MaskT, kCountOnly, 1>(a, L, s); break;
     }
 }
 

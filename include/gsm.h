@@ -163,7 +163,8 @@ enum {
     GSM_K_SCAN = 3,     /* work scan (CUB) + merge-path partition        */
     GSM_K_EXPAND = 4,   /* K2/K3/K4 expand + verify + compact            */
     GSM_K_FINALIZE = 5, /* id map, Aut expansion, radix sort             */
-    GSM_K_COUNT_ = 6
+    GSM_K_TAIL = 6,     /* fused last two positions (COUNT mode, clique-like tails) */
+    GSM_K_COUNT_ = 7
 };
 
 typedef struct {

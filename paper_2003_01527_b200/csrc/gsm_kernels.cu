@@ -276,13 +276,13 @@ __global__ void __launch_bounds__(kThreads) k_plan_rows(const int32_t* __restric
                 admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, false, s0, t0);
                 if (t0 - s0 < blen) { blen = t0 - s0; bq = q; }
             }
-            // exact segments: the pivot's (its length is the work of this row) and the
-            // membership lists of the other backward neighbours (searched per candidate)
+            // exact segments: the pivot's (its length is the work of this row; exact bounds
+            // mean the expand kernel never re-checks the ID constraints) and the membership
+            // lists of the other backward neighbours (searched per candidate)
             for (int q = 0; q < nb; ++q) {
                 int64_t s0, t0;
                 const bool pivot = q == bq;
-                admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, !empty && (pivot ? blen > 8 : true),
-                                   s0, t0);
+                admissible_segment(off, cols, up, n, row[L.bpos[q]], lov, hiv, !empty, s0, t0);
                 if (empty) t0 = s0;
                 cbeg[r * nb + q] = s0;
                 clen[r * nb + q] = (int32_t)(t0 - s0);
@@ -517,13 +517,16 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
                     v[j] = cols[sBeg[lr[j]] + ((ib0 + xi) - sP[lr[j]])] & L.idmask;
                 }
             }
+            // (ID bounds need no test: plan_rows cut every pivot segment to the exact open
+            //  interval of admissible ids; only positions neither adjacent nor bounded need
+            //  an explicit injectivity compare)
+            if (L.ninj) {
 #pragma unroll
-            for (int j = 0; j < U; ++j) {
-                if (!ok[j]) continue;
-                const int32_t* row = sRow + lr[j] * W;
-                for (int q = 0; q < L.nlo && ok[j]; ++q) ok[j] = v[j] > row[L.lo[q]];
-                for (int q = 0; q < L.nhi && ok[j]; ++q) ok[j] = v[j] < row[L.hi[q]];
-                for (int q = 0; q < L.ninj && ok[j]; ++q) ok[j] = v[j] != row[L.inj[q]];
+                for (int j = 0; j < U; ++j) {
+                    if (!ok[j]) continue;
+                    const int32_t* row = sRow + lr[j] * W;
+                    for (int q = 0; q < L.ninj && ok[j]; ++q) ok[j] = v[j] != row[L.inj[q]];
+                }
             }
             if (L.check_mask) {
                 uint32_t m[U];
@@ -675,6 +678,168 @@ void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cuda
         case 2: c ? launch_expand_t<uint16_t, true>(a, L, s) : launch_expand_t<uint16_t, false>(a, L, s); break;
         default: c ? launch_expand_t<uint32_t, true>(a, L, s) : launch_expand_t<uint32_t, false>(a, L, s); break;
     }
+}
+
+// ============================================================================
+// Fused tail (COUNT mode, last two positions k-2 and k-1) — candidate-set
+// inheritance.  When π[k-1] is adjacent to π[k-2] and to every backward
+// neighbour of π[k-2] (B(k-1) = B(k-2) ∪ {k-2}, e.g. cliques), with the same
+// label and no looser ID bounds, the raw candidate set of position k-2,
+//   RC(r) = ∩_{j in B(k-2)} N(f(j))  within the ID interval of position k-2,
+// also contains every admissible image of π[k-1]; so one warp per partial
+// result r builds RC(r) once in shared memory (Advance + Compute of position
+// k-2) and counts, for every c in RC(r) that passes position k-2's
+// own tests, the d in RC(r) with d ∈ N(c) (position k-1's one remaining
+// connection check) — the level-(k-1) frontier is never written to HBM.
+// Per c the cheaper side is enumerated: RC's entries searched in N(c) (global
+// binary search), or N(c)'s admissible part searched in RC (shared memory).
+// Rows whose pivot segment exceeds the per-warp buffer are handed back (overflow
+// list) to the generic BFS path.
+// ============================================================================
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, LevelPlan Ld) {
+    extern __shared__ __align__(16) int32_t tail_smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    int32_t* rc = tail_smem + wib * a.cap;
+    const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
+    const int32_t* __restrict__ cols = a.cols;
+    const int W = Lc.width;
+    const int nb = Lc.nb;
+    const int32_t kb = Lc.key_base, idm = Lc.idmask;
+    unsigned long long cnt = 0, items = 0, probes_u = 0;
+    unsigned probes = 0;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = gw; r < a.R; r += nw) {
+        const int64_t len = a.rlen[r];
+        if (len == 0) continue;
+        if (len > a.cap) {
+            if (lane == 0) a.overflow[atomicAdd(a.noverflow, 1ull)] = r;
+            continue;
+        }
+        const int32_t* row = a.F + r * W;
+        const int piv = a.rpiv[r];
+        const int64_t beg = a.rbeg[r];
+        // ---- phase 1: RC(r) = pivot entries present in every other backward list (order kept)
+        int n = 0;
+        for (int64_t base = 0; base < len; base += 32) {
+            const int64_t i = base + lane;
+            bool ok = i < len;
+            int32_t v = ok ? (cols[beg + i] & idm) : 0;
+            if (ok) ++items;
+            for (int q = 0; q < nb && ok; ++q) {
+                if (q == piv) continue;
+                ok = in_sorted(cols + a.cbeg[r * nb + q], a.clen[r * nb + q], kb | v, probes);
+            }
+            const unsigned ball = __ballot_sync(0xffffffffu, ok);
+            if (ok) rc[n + __popc(ball & ((1u << lane) - 1u))] = v;
+            n += __popc(ball);
+        }
+        __syncwarp();
+        // ---- phase 2: pairs (c, d) inside RC(r)
+        for (int i = 0; i < n; ++i) {
+            const int32_t c = rc[i];
+            bool okc = true;
+            if (Lc.check_mask) okc = (cmask[c] >> Lc.qv) & 1u;
+            for (int q = 0; q < Lc.ninj && okc; ++q) okc = c != row[Lc.inj[q]];
+            if (!okc) continue;  // warp-uniform
+            int j0 = 0, j1 = n;
+            if (a.rel > 0) j0 = i + 1;
+            else if (a.rel < 0) j1 = i;
+            if (j1 <= j0) continue;
+            const int64_t cs = a.off[c], ce = a.off[c + 1];
+            const int64_t s0 = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rc[j0]));
+            const int64_t t0 = lower_bound_cols(cols, s0, ce, (int64_t)(kb | rc[j1 - 1]) + 1);
+            const int64_t nA = j1 - j0, nB = t0 - s0;
+            if (nB <= 0) continue;
+            if (nA <= nB) {
+                for (int j = j0 + lane; j < j1; j += 32) {
+                    if (j == i) continue;
+                    const int32_t d = rc[j];
+                    ++items;
+                    bool ok = true;
+                    if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                    for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                    for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                    for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                    if (ok) ok = in_sorted(cols + s0, (int)nB, kb | d, probes);
+                    cnt += ok;
+                }
+            } else {
+                for (int64_t x = s0 + lane; x < t0; x += 32) {
+                    const int32_t d = cols[x] & idm;
+                    ++items;
+                    unsigned dummy = 0;
+                    bool ok = d != c && in_sorted(rc + j0, j1 - j0, d, dummy);
+                    if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                    for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                    for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                    for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                    cnt += ok;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    probes_u = probes;
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        items += __shfl_xor_sync(0xffffffffu, items, o);
+        probes_u += __shfl_xor_sync(0xffffffffu, probes_u, o);
+    }
+    if (lane == 0) {
+        if (cnt) {
+            atomicAdd(a.count, cnt);
+            atomicAdd(&a.stats[3], cnt);
+        }
+        if (items) atomicAdd(&a.stats[0], items);
+        if (probes_u) atomicAdd(&a.stats[2], probes_u);
+    }
+}
+
+int tail_cap() {  // per-warp candidate buffer; GSM_TAIL_CAP (tests force the overflow path with it)
+    const char* v = getenv("GSM_TAIL_CAP");
+    int cap = (v && *v) ? atoi(v) : 1024;
+    if (cap < 32) cap = 32;
+    if (cap > 6144) cap = 6144;
+    return cap;
+}
+
+template <typename MaskT>
+static void launch_tail_t(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, cudaStream_t s) {
+    const size_t smem = sizeof(int32_t) * (size_t)a.cap * kWarps;
+    GSM_CUDA(cudaFuncSetAttribute(k_tail<MaskT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    int dev = 0, sms = 148, per_sm = 1;
+    GSM_CUDA(cudaGetDevice(&dev));
+    GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail<MaskT>, kThreads, smem));
+    const int64_t want = (a.R + kWarps - 1) / kWarps;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1)));
+    k_tail<MaskT><<<(unsigned)grid, kThreads, smem, s>>>(a, Lc, Ld);
+    GSM_LAUNCH("k_tail");
+}
+
+void launch_tail(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s) {
+    switch (mask_bytes) {
+        case 1: launch_tail_t<uint8_t>(a, Lc, Ld, s); break;
+        case 2: launch_tail_t<uint16_t>(a, Lc, Ld, s); break;
+        default: launch_tail_t<uint32_t>(a, Lc, Ld, s); break;
+    }
+}
+
+__global__ void k_gather_overflow(const int32_t* __restrict__ F, int W, const int64_t* __restrict__ idx, int64_t n,
+                                  int32_t* __restrict__ out) {
+    const int64_t total = n * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / W;
+        out[i] = F[idx[r] * W + (i - r * W)];
+    }
+}
+
+void launch_gather_rows(const int32_t* F, int W, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s) {
+    k_gather_overflow<<<grid_for(n * W), kThreads, 0, s>>>(F, W, idx, n, out);
+    GSM_LAUNCH("k_gather_overflow");
 }
 
 // ============================================================================

@@ -71,6 +71,31 @@ int64_t expand_tile(int width);
 // K2+K3+K4 fused: expand + verify + compact (Alg. 1 lines 11-13).
 void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cudaStream_t s);
 
+// Fused tail (COUNT mode): positions k-2 and k-1 in one kernel (candidate-set inheritance).
+struct TailArgs {
+    const int32_t* F;       // rows of width k-2
+    int64_t R;
+    const int64_t* rbeg;    // plan of position k-2 (k_plan_rows)
+    const int64_t* rlen;
+    const uint8_t* rpiv;
+    const int64_t* cbeg;
+    const int32_t* clen;
+    const int64_t* off;
+    const int32_t* cols;    // plain or keyed lists (same as position k-2's)
+    const void* cmask;
+    int32_t rel;            // +1: f(π[k-1]) ≻ f(π[k-2]); -1: ≺; 0: unconstrained
+    int32_t cap;            // per-warp candidate buffer (int32 entries)
+    int32_t nxlo, nxhi;     // extra ID bounds of π[k-1] not implied by π[k-2]'s interval
+    int32_t xlo[kMaxK], xhi[kMaxK];
+    unsigned long long* count;
+    int64_t* overflow;      // rows left to the generic path
+    unsigned long long* noverflow;
+    unsigned long long* stats;
+};
+int tail_cap();
+void launch_tail(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s);
+void launch_gather_rows(const int32_t* F, int W, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s);
+
 // Finalize ("Return ... subgraph enumeration M").
 void launch_to_query_order(const int32_t* in, int64_t N, int k, const int32_t* order, const int32_t* new2old,
                            int32_t* out, cudaStream_t s);

@@ -104,6 +104,9 @@ class Matcher {
 
    private:
     void process(int w, const int32_t* F, int64_t R);
+    void process_generic(int w, const int32_t* F, int64_t R);
+    void process_tail(int w, const int32_t* F, int64_t R);
+    bool tail_eligible(TailArgs* ta) const;
     void append_output(const int32_t* rows, int64_t R);
     void finalize();
 
@@ -126,6 +129,12 @@ class Matcher {
     int64_t arena_rows_ = 0;
     int64_t budget_ = 0;
     double t_expand_ms_ = 0;
+    bool tail_ = false;        // fuse the last two positions (COUNT mode)
+    TailArgs tail_args_;
+    double tail_rows_ = 0;     // rows handled by the fused tail
+    DevBuf<int64_t> ovf_idx_;
+    DevBuf<int32_t> ovf_rows_;
+    DevBuf<unsigned long long> ovf_n_;
 };
 
 void Matcher::run() {
@@ -179,6 +188,8 @@ void Matcher::run() {
             L.check_mask = plan_.qdeg[L.qv] > L.nb ? 1 : 0;  // the label is implied by the key range
         }
     }
+
+    tail_ = tail_eligible(&tail_args_);
 
     // ---- roots = C(π[0]) (level-0 frontier)
     int64_t R0 = 0;
@@ -253,7 +264,16 @@ void Matcher::run() {
             res_->level_rows[w] = st[3];  // partial results with w+1 matched positions
         }
         res_->prof[GSM_K_EXPAND].alg_bytes += eb;
+        if (tail_) {
+            const unsigned long long* st = hs.data() + 5 * kMaxK;
+            const int w = k_ - 2;
+            const LevelPlan& L = lplan_[w];
+            res_->prof[GSM_K_TAIL].alg_bytes +=
+                tail_rows_ * (4.0 * w + 8 + 8 + 1 + 12.0 * L.nb) + 4.0 * st[0] + 4.0 * st[2];
+            res_->level_work[k_ - 1] += st[0];
+        }
     }
+    if (k_ > 1 && count_mode_) res_->level_rows[k_ - 1] = found;
     res_->count_unique = found;
     const bool expand_orbits = plan_.symmetric && !(opts_.flags & GSM_FLAG_UNIQUE);
     res_->count = expand_orbits ? found * plan_.aut_size : found;
@@ -268,6 +288,86 @@ void Matcher::run() {
 }
 
 void Matcher::process(int w, const int32_t* F, int64_t R) {
+    if (R <= 0) return;
+    if (tail_ && w == k_ - 2) process_tail(w, F, R);
+    else process_generic(w, F, R);
+}
+
+// Eligibility of the fused tail: COUNT mode; B(k-1) = B(k-2) ∪ {k-2}; π[k-1] has the
+// label of π[k-2] (or Q is unlabeled); π[k-1]'s ID bounds from earlier positions
+// include π[k-2]'s (so RC(r) holds every admissible image of π[k-1]).
+bool Matcher::tail_eligible(TailArgs* ta) const {
+    const char* env = getenv("GSM_FUSED_TAIL");
+    if (env && env[0] == '0') return false;
+    if (!count_mode_ || k_ < 3) return false;
+    const int c = k_ - 2, d = k_ - 1;
+    if (plan_.backward[d] != (plan_.backward[c] | (1u << c))) return false;
+    if (plan_.use_labels && plan_.qlabel[plan_.order[c]] != plan_.qlabel[plan_.order[d]]) return false;
+    const LevelPlan &Lc = lplan_[c], &Ld = lplan_[d];
+    if (Lc.keyed != Ld.keyed) return false;
+    auto has = [](const int32_t* a, int n, int x) {
+        for (int i = 0; i < n; ++i)
+            if (a[i] == x) return true;
+        return false;
+    };
+    for (int i = 0; i < Lc.nlo; ++i)
+        if (!has(Ld.lo, Ld.nlo, Lc.lo[i])) return false;
+    for (int i = 0; i < Lc.nhi; ++i)
+        if (!has(Ld.hi, Ld.nhi, Lc.hi[i])) return false;
+    std::memset(ta, 0, sizeof(*ta));
+    ta->rel = has(Ld.lo, Ld.nlo, c) ? 1 : (has(Ld.hi, Ld.nhi, c) ? -1 : 0);
+    for (int i = 0; i < Ld.nlo; ++i)
+        if (Ld.lo[i] != c && !has(Lc.lo, Lc.nlo, Ld.lo[i])) ta->xlo[ta->nxlo++] = Ld.lo[i];
+    for (int i = 0; i < Ld.nhi; ++i)
+        if (Ld.hi[i] != c && !has(Lc.hi, Lc.nhi, Ld.hi[i])) ta->xhi[ta->nxhi++] = Ld.hi[i];
+    return true;
+}
+
+void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
+    LevelBufs& B = *lv_[w];
+    const LevelPlan& L = lplan_[w];
+    B.rbeg.ensure(R, s_);
+    B.rlen.ensure(R, s_);
+    B.rpiv.ensure(R, s_);
+    B.cbeg.ensure((size_t)R * L.nb, s_);
+    B.clen.ensure((size_t)R * L.nb, s_);
+    rec_.run(GSM_K_PLAN, 1, [&] { launch_plan_rows(g_, F, R, L, B.rbeg.p, B.rlen.p, B.rpiv.p, B.cbeg.p, B.clen.p, s_); });
+    res_->prof[GSM_K_PLAN].alg_bytes += (double)R * (4.0 * w + 16.0 * L.nb + 12.0 * L.nb + 8 + 8 + 1);
+    ovf_idx_.ensure(R, s_);
+    ovf_n_.ensure(1, s_);
+    GSM_CUDA(cudaMemsetAsync(ovf_n_.p, 0, sizeof(unsigned long long), s_));
+    TailArgs a = tail_args_;
+    a.F = F;
+    a.R = R;
+    a.rbeg = B.rbeg.p;
+    a.rlen = B.rlen.p;
+    a.rpiv = B.rpiv.p;
+    a.cbeg = B.cbeg.p;
+    a.clen = B.clen.p;
+    a.off = g_.off;
+    a.cols = L.keyed ? g_.lkeys : g_.cols;
+    a.cmask = cmask_.p;
+    a.cap = tail_cap();
+    a.count = final_count_.p;
+    a.overflow = ovf_idx_.p;
+    a.noverflow = ovf_n_.p;
+    a.stats = stats_.p + 5 * (kMaxK + 0);  // tail counters: slot kMaxK
+    rec_.run(GSM_K_TAIL, 1, [&] { launch_tail(a, L, lplan_[w + 1], mask_bytes_, s_); });
+    res_->num_chunks++;
+    tail_rows_ += (double)R;
+    const int64_t nov = (int64_t)read_scalar(ovf_n_.p, s_);
+    if (nov > 0) {  // rows whose candidate list did not fit the per-warp buffer
+        ovf_rows_.ensure((size_t)nov * w, s_);
+        launch_gather_rows(F, w, ovf_idx_.p, nov, ovf_rows_.p, s_);
+        res_->kernel_launches++;
+        DevBuf<int32_t> rows;
+        rows.ensure((size_t)nov * w, s_);
+        GSM_CUDA(cudaMemcpyAsync(rows.p, ovf_rows_.p, sizeof(int32_t) * nov * w, cudaMemcpyDeviceToDevice, s_));
+        process_generic(w, rows.p, nov);
+    }
+}
+
+void Matcher::process_generic(int w, const int32_t* F, int64_t R) {
     if (R <= 0) return;
     LevelBufs& B = *lv_[w];
     const LevelPlan& L = lplan_[w];

@@ -117,6 +117,29 @@ def test_labeled_named_queries():
         G.free()
 
 
+@pytest.mark.parametrize("tail", ["0", "1", "cap32"])
+def test_fused_tail_matches_generic_path(tail, monkeypatch):
+    """The fused last-two-positions kernel (COUNT mode, clique-like tails) against the
+    oracle, with the fusion disabled, enabled, and enabled with a tiny per-warp buffer
+    (forcing the overflow hand-back to the generic path)."""
+    monkeypatch.setenv("GSM_FUSED_TAIL", "0" if tail == "0" else "1")
+    if tail == "cap32":
+        monkeypatch.setenv("GSM_TAIL_CAP", "32")
+    g = gi.rmat(10, 16, seed=12).with_labels(gi.uniform_labels(1024, 2, 12))
+    G = load(g)
+    try:
+        for q in [gi.query("K3"), gi.query("K4"), gi.query("K3", [0, 0, 0]), gi.query("K3", [0, 0, 1]),
+                  gi.query("K4", [1, 1, 1, 1]), gi.query("diamond"), gi.query("tailed_triangle"), gi.query("K2"),
+                  gi.Query(5, [(a, b) for a in range(5) for b in range(a + 1, 5)], None, "K5")]:
+            cnt, _ = oracle.match(g, q, count_only=True)
+            for flags in (0, gsm.GSM_FLAG_UNIQUE, gsm.GSM_FLAG_NO_SYMMETRY):
+                c, _, r = run(G, q, "count", flags=flags)
+                want = cnt if flags != gsm.GSM_FLAG_UNIQUE else cnt // r.automorphisms
+                assert c == want, (tail, q.name, flags, c, want)
+    finally:
+        G.free()
+
+
 def test_closed_forms_on_gpu():
     for n in (5, 8):
         G = load(gi.complete(n))

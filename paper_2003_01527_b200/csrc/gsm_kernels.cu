@@ -628,6 +628,168 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
     }
 }
 
+// ============================================================================
+// Last position in COUNT mode: "walking" variant of the expand kernel.
+// Each thread owns VT consecutive merge-path steps of the tile, found by one
+// shared-memory merge-path search, and walks them serially: the candidates it
+// sees inside one row are consecutive entries of the sorted pivot segment, so
+// every membership test gallops forward from the previous hit (exponential
+// then binary search) instead of restarting a full binary search — O(log gap)
+// per candidate, no per-candidate row lookup, two barriers per tile, and only
+// the tile's row ends staged in shared memory.  Nothing is written.
+// ============================================================================
+constexpr int kWalkVT = 16;
+constexpr int kWalkMaxNb = 4;
+
+bool use_walk(const LevelPlan& L) {
+    const char* v = getenv("GSM_COUNT_WALK");
+    if (v && v[0] == '0') return false;
+    return L.count_only && L.nb <= kWalkMaxNb;
+}
+
+int64_t expand_tile_for(const LevelPlan& L) {
+    return use_walk(L) ? (int64_t)kThreads * kWalkVT : expand_tile(L.width);
+}
+
+// first index in [p, e) with a[idx] >= key, galloping from p
+__device__ __forceinline__ int64_t gallop(const int32_t* __restrict__ a, int64_t p, int64_t e, int32_t key,
+                                          unsigned& probes) {
+    if (p >= e) return e;
+    ++probes;
+    if (a[p] >= key) return p;
+    int64_t lo = p, step = 1;  // invariant: a[lo] < key
+    while (lo + step < e) {
+        ++probes;
+        if (a[lo + step] >= key) break;
+        lo += step;
+        step <<= 1;
+    }
+    int64_t hi = min(lo + step, e);  // answer in (lo, hi]
+    ++lo;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        ++probes;
+        if (a[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_count_walk(ExpandArgs a, LevelPlan L) {
+    extern __shared__ __align__(16) int64_t sA[];  // row ends P[r+1] of the tile's rows
+    const int64_t TD = a.TD;
+    const int W = L.width;
+    const int nb = L.nb;
+    const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
+    const int32_t* __restrict__ cols = a.cols;
+    unsigned long long cnt = 0;
+    unsigned st_items = 0, st_mask = 0, st_probes = 0, st_lists = 0;
+    for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const int64_t d0 = a.D0 + t * TD;
+        const int64_t d1 = min(d0 + TD, a.D1);
+        const int64_t ra0 = a.tile_ra[t], ra1 = a.tile_ra[t + 1];
+        if (d1 - ra1 <= d0 - ra0) continue;  // no candidates in this tile (block-uniform)
+        const int64_t rlast = min(ra1, a.R - 1);
+        const int nrows = (int)(rlast - ra0 + 1);
+        __syncthreads();
+        for (int i = threadIdx.x; i < nrows; i += kThreads) sA[i] = a.P[ra0 + i + 1];
+        __syncthreads();
+        const int64_t d = d0 + (int64_t)threadIdx.x * kWalkVT;
+        if (d >= d1) continue;
+        // merge-path split for diagonal d inside [ra0, ra1]
+        int64_t lo = ra0, hi = min(ra1, d);
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (sA[mid - ra0] <= d - mid - 1) lo = mid + 1; else hi = mid;
+        }
+        int64_t r = lo, x = d - lo;
+        const int64_t dend = min(d + kWalkVT, d1);
+        int64_t cur = -1, beg = 0, base = 0;
+        int piv = 0;
+        int64_t cpos[kWalkMaxNb], cend[kWalkMaxNb];
+        for (int64_t step = d; step < dend; ++step) {
+            if (r > rlast) break;
+            if (sA[r - ra0] <= x) {  // row r ends before item x: consume the row end
+                ++r;
+                continue;
+            }
+            if (r != cur) {  // entering row r: its pivot segment and membership segments
+                cur = r;
+                beg = a.rbeg[r];
+                base = (r == ra0) ? a.P[r] : sA[r - 1 - ra0];
+                piv = a.rpiv[r];
+#pragma unroll
+                for (int q = 0; q < kWalkMaxNb; ++q) {
+                    if (q < nb) {
+                        cpos[q] = a.cbeg[r * nb + q];
+                        cend[q] = cpos[q] + a.clen[r * nb + q];
+                    }
+                }
+            }
+            ++st_items;
+            const int32_t v = cols[beg + (x - base)] & L.idmask;
+            ++x;
+            bool ok = true;
+            if (L.check_mask) {
+                ++st_mask;
+                ok = (cmask[v] >> L.qv) & 1u;
+            }
+            if (ok && L.ninj) {
+                const int32_t* row = a.F + r * W;
+                for (int q = 0; q < L.ninj && ok; ++q) ok = v != row[L.inj[q]];
+            }
+            const int32_t key = L.key_base | v;
+#pragma unroll
+            for (int q = 0; q < kWalkMaxNb; ++q) {
+                if (q < nb && q != piv && ok) {
+                    ++st_lists;
+                    cpos[q] = gallop(cols, cpos[q], cend[q], key, st_probes);
+                    ok = cpos[q] < cend[q] && cols[cpos[q]] == key;
+                }
+            }
+            cnt += ok;
+        }
+    }
+    // block reduction of the counters (same layout as k_expand)
+    __shared__ unsigned long long sRed[kWarps][5];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long v5[5] = {cnt, st_items, st_mask, st_probes, st_lists};
+#pragma unroll
+    for (int c = 0; c < 5; ++c)
+        for (int o = 16; o; o >>= 1) v5[c] += __shfl_xor_sync(0xffffffffu, v5[c], o);
+    __syncthreads();
+    if (lane == 0)
+        for (int c = 0; c < 5; ++c) sRed[warp][c] = v5[c];
+    __syncthreads();
+    if (threadIdx.x < 5) {
+        unsigned long long sum = 0;
+        for (int w = 0; w < kWarps; ++w) sum += sRed[w][threadIdx.x];
+        if (sum) {
+            if (threadIdx.x == 0) {
+                atomicAdd(a.out_count, sum);
+                atomicAdd(&a.stats[3], sum);
+            } else if (threadIdx.x < 4) {
+                atomicAdd(&a.stats[threadIdx.x - 1], sum);
+            } else {
+                atomicAdd(&a.stats[4], sum);
+            }
+        }
+    }
+}
+
+template <typename MaskT>
+static void launch_walk_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
+    const size_t smem = sizeof(int64_t) * (size_t)(a.TD + 1);
+    GSM_CUDA(cudaFuncSetAttribute(k_count_walk<MaskT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    int dev = 0, sms = 148, per_sm = 1;
+    GSM_CUDA(cudaGetDevice(&dev));
+    GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_walk<MaskT>, kThreads, smem));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(a.ntiles, (int64_t)sms * std::max(per_sm, 1)));
+    k_count_walk<MaskT><<<(unsigned)grid, kThreads, smem, s>>>(a, L);
+    GSM_LAUNCH("k_count_walk");
+}
+
 static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return (v && *v) ? atoi(v) : dflt;
@@ -672,6 +834,14 @@ static void launch_expand_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_
 }
 
 void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cudaStream_t s) {
+    if (use_walk(L) && a.TD == (int64_t)kThreads * kWalkVT) {
+        switch (mask_bytes) {
+            case 1: launch_walk_t<uint8_t>(a, L, s); break;
+            case 2: launch_walk_t<uint16_t>(a, L, s); break;
+            default: launch_walk_t<uint32_t>(a, L, s); break;
+        }
+        return;
+    }
     const bool c = L.count_only != 0;
     switch (mask_bytes) {
         case 1: c ? launch_expand_t<uint8_t, true>(a, L, s) : launch_expand_t<uint8_t, false>(a, L, s); break;

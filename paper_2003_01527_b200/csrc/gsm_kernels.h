@@ -65,8 +65,10 @@ struct ExpandArgs {
     unsigned long long* stats;      // [items, mask_checked, probes, survivors, lists]
 };
 
-// Tile size (merge steps per CTA) for a given input width.
+// Tile size (merge steps per CTA) for a given input width / for a level plan (the COUNT-mode
+// last level uses the walking kernel with its own, larger tile).
 int64_t expand_tile(int width);
+int64_t expand_tile_for(const LevelPlan& L);
 
 // K2+K3+K4 fused: expand + verify + compact (Alg. 1 lines 11-13).
 void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cudaStream_t s);

@@ -388,7 +388,7 @@ void Matcher::process_generic(int w, const int32_t* F, int64_t R) {
     if (S <= 0) return;
 
     const int64_t total = R + S;
-    const int64_t TD = expand_tile(w);
+    const int64_t TD = expand_tile_for(L);
     const bool last = (w == k_ - 1);
     int64_t chunk;
     if (last && count_mode_) {

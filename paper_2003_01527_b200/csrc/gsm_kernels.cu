@@ -968,6 +968,149 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
     }
 }
 
+// Big rows of the fused tail: one CTA per row, RC(r) (up to a.cap entries) built
+// block-wide in shared memory (order-preserving ballot compaction with a warp
+// scan per 256-candidate round), then the 8 warps split the c's of RC(r).
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan Lc, LevelPlan Ld) {
+    extern __shared__ __align__(16) int32_t rcb[];
+    __shared__ int sWarpCnt[kWarps];
+    __shared__ int sN;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
+    const int32_t* __restrict__ cols = a.cols;
+    const int W = Lc.width;
+    const int nb = Lc.nb;
+    const int32_t kb = Lc.key_base, idm = Lc.idmask;
+    unsigned long long cnt = 0, items = 0;
+    unsigned probes = 0;
+    for (int64_t ri = blockIdx.x; ri < a.R; ri += gridDim.x) {
+        const int64_t r = a.rows_idx ? a.rows_idx[ri] : ri;
+        const int64_t len = a.rlen[r];
+        if (len == 0) continue;  // block-uniform
+        if (len > a.cap) {
+            if (threadIdx.x == 0) a.overflow[atomicAdd(a.noverflow, 1ull)] = r;
+            continue;
+        }
+        const int32_t* row = a.F + r * W;
+        const int piv = a.rpiv[r];
+        const int64_t beg = a.rbeg[r];
+        __syncthreads();
+        if (threadIdx.x == 0) sN = 0;
+        __syncthreads();
+        for (int64_t base = 0; base < len; base += kThreads) {
+            const int64_t i = base + threadIdx.x;
+            bool ok = i < len;
+            const int32_t v = ok ? (cols[beg + i] & idm) : 0;
+            if (ok) ++items;
+            for (int q = 0; q < nb && ok; ++q) {
+                if (q == piv) continue;
+                ok = in_sorted(cols + a.cbeg[r * nb + q], a.clen[r * nb + q], kb | v, probes);
+            }
+            const unsigned ball = __ballot_sync(0xffffffffu, ok);
+            if (lane == 0) sWarpCnt[warp] = __popc(ball);
+            __syncthreads();
+            int off = sN;
+            for (int w = 0; w < warp; ++w) off += sWarpCnt[w];
+            if (ok) rcb[off + __popc(ball & ((1u << lane) - 1u))] = v;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int tot = 0;
+                for (int w = 0; w < kWarps; ++w) tot += sWarpCnt[w];
+                sN += tot;
+            }
+            __syncthreads();
+        }
+        const int n = sN;
+        for (int i = warp; i < n; i += kWarps) {
+            const int32_t c = rcb[i];
+            bool okc = true;
+            if (Lc.check_mask) okc = (cmask[c] >> Lc.qv) & 1u;
+            for (int q = 0; q < Lc.ninj && okc; ++q) okc = c != row[Lc.inj[q]];
+            if (!okc) continue;
+            int j0 = 0, j1 = n;
+            if (a.rel > 0) j0 = i + 1;
+            else if (a.rel < 0) j1 = i;
+            if (j1 <= j0) continue;
+            const int64_t cs = a.off[c], ce = a.off[c + 1];
+            const int64_t s0 = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rcb[j0]));
+            const int64_t t0 = lower_bound_cols(cols, s0, ce, (int64_t)(kb | rcb[j1 - 1]) + 1);
+            const int64_t nA = j1 - j0, nB = t0 - s0;
+            if (nB <= 0) continue;
+            if (nA <= nB) {
+                for (int j = j0 + lane; j < j1; j += 32) {
+                    if (j == i) continue;
+                    const int32_t d = rcb[j];
+                    ++items;
+                    bool ok = true;
+                    if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                    for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                    for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                    for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                    if (ok) ok = in_sorted(cols + s0, (int)nB, kb | d, probes);
+                    cnt += ok;
+                }
+            } else {
+                for (int64_t x = s0 + lane; x < t0; x += 32) {
+                    const int32_t d = cols[x] & idm;
+                    ++items;
+                    unsigned dummy = 0;
+                    bool ok = d != c && in_sorted(rcb + j0, j1 - j0, d, dummy);
+                    if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                    for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                    for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                    for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                    cnt += ok;
+                }
+            }
+        }
+    }
+    unsigned long long probes_u = probes;
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        items += __shfl_xor_sync(0xffffffffu, items, o);
+        probes_u += __shfl_xor_sync(0xffffffffu, probes_u, o);
+    }
+    if (lane == 0) {
+        if (cnt) {
+            atomicAdd(a.count, cnt);
+            atomicAdd(&a.stats[3], cnt);
+        }
+        if (items) atomicAdd(&a.stats[0], items);
+        if (probes_u) atomicAdd(&a.stats[2], probes_u);
+    }
+}
+
+template <typename MaskT>
+static void launch_tail_block_t(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, cudaStream_t s) {
+    const size_t smem = sizeof(int32_t) * (size_t)a.cap;
+    GSM_CUDA(cudaFuncSetAttribute(k_tail_block<MaskT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    int dev = 0, sms = 148, per_sm = 1;
+    GSM_CUDA(cudaGetDevice(&dev));
+    GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_block<MaskT>, kThreads, smem));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(a.R, (int64_t)sms * std::max(per_sm, 1)));
+    k_tail_block<MaskT><<<(unsigned)grid, kThreads, smem, s>>>(a, Lc, Ld);
+    GSM_LAUNCH("k_tail_block");
+}
+
+void launch_tail_block(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s) {
+    switch (mask_bytes) {
+        case 1: launch_tail_block_t<uint8_t>(a, Lc, Ld, s); break;
+        case 2: launch_tail_block_t<uint16_t>(a, Lc, Ld, s); break;
+        default: launch_tail_block_t<uint32_t>(a, Lc, Ld, s); break;
+    }
+}
+
+int tail_block_cap() {  // per-CTA buffer for big rows (GSM_TAIL_BLOCK_CAP)
+    const char* v = getenv("GSM_TAIL_BLOCK_CAP");
+    int cap = (v && *v) ? atoi(v) : 40960;
+    if (cap < 256) cap = 256;
+    if (cap > 48 * 1024) cap = 48 * 1024;
+    return cap;
+}
+
 int tail_cap() {  // per-warp candidate buffer; GSM_TAIL_CAP (tests force the overflow path with it)
     const char* v = getenv("GSM_TAIL_CAP");
     int cap = (v && *v) ? atoi(v) : 1024;

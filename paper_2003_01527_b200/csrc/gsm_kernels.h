@@ -90,11 +90,14 @@ struct TailArgs {
     int32_t nxlo, nxhi;     // extra ID bounds of π[k-1] not implied by π[k-2]'s interval
     int32_t xlo[kMaxK], xhi[kMaxK];
     unsigned long long* count;
-    int64_t* overflow;      // rows left to the generic path
+    const int64_t* rows_idx;  // k_tail_block: indices of the rows to process (NULL = 0..R-1)
+    int64_t* overflow;      // rows left to the next stage
     unsigned long long* noverflow;
     unsigned long long* stats;
 };
 int tail_cap();
+int tail_block_cap();
+void launch_tail_block(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s);
 void launch_tail(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s);
 void launch_gather_rows(const int32_t* F, int W, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s);
 

@@ -355,8 +355,21 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
     rec_.run(GSM_K_TAIL, 1, [&] { launch_tail(a, L, lplan_[w + 1], mask_bytes_, s_); });
     res_->num_chunks++;
     tail_rows_ += (double)R;
-    const int64_t nov = (int64_t)read_scalar(ovf_n_.p, s_);
-    if (nov > 0) {  // rows whose candidate list did not fit the per-warp buffer
+    int64_t nov = (int64_t)read_scalar(ovf_n_.p, s_);
+    if (nov > 0) {  // rows whose list did not fit a warp's buffer: one CTA per row
+        DevBuf<int64_t> idx;
+        idx.ensure(nov, s_);
+        GSM_CUDA(cudaMemcpyAsync(idx.p, ovf_idx_.p, sizeof(int64_t) * nov, cudaMemcpyDeviceToDevice, s_));
+        GSM_CUDA(cudaMemsetAsync(ovf_n_.p, 0, sizeof(unsigned long long), s_));
+        TailArgs b = a;
+        b.R = nov;
+        b.rows_idx = idx.p;
+        b.cap = tail_block_cap();
+        rec_.run(GSM_K_TAIL, 1, [&] { launch_tail_block(b, L, lplan_[w + 1], mask_bytes_, s_); });
+        res_->num_chunks++;
+        nov = (int64_t)read_scalar(ovf_n_.p, s_);
+    }
+    if (nov > 0) {  // still too big for a CTA: generic breadth-first path
         ovf_rows_.ensure((size_t)nov * w, s_);
         launch_gather_rows(F, w, ovf_idx_.p, nov, ovf_rows_.p, s_);
         res_->kernel_launches++;

@@ -117,14 +117,16 @@ def test_labeled_named_queries():
         G.free()
 
 
-@pytest.mark.parametrize("tail", ["0", "1", "cap32"])
+@pytest.mark.parametrize("tail", ["0", "1", "cap32", "cap32block256"])
 def test_fused_tail_matches_generic_path(tail, monkeypatch):
     """The fused last-two-positions kernel (COUNT mode, clique-like tails) against the
     oracle, with the fusion disabled, enabled, and enabled with a tiny per-warp buffer
     (forcing the overflow hand-back to the generic path)."""
     monkeypatch.setenv("GSM_FUSED_TAIL", "0" if tail == "0" else "1")
-    if tail == "cap32":
+    if tail.startswith("cap32"):
         monkeypatch.setenv("GSM_TAIL_CAP", "32")
+    if tail == "cap32block256":
+        monkeypatch.setenv("GSM_TAIL_BLOCK_CAP", "256")
     g = gi.rmat(10, 16, seed=12).with_labels(gi.uniform_labels(1024, 2, 12))
     G = load(g)
     try:
@@ -333,8 +335,9 @@ def test_device_pointer_load_and_profile():
     try:
         c, _, r = run(G, gi.query("K3"), flags=gsm.GSM_FLAG_PROFILE)
         assert c == 6 * oracle.count_triangles(g)
-        assert r.prof["expand"]["launches"] >= 1 and r.prof["expand"]["ms"] > 0
-        assert r.prof["expand"]["alg_bytes"] > 0 and r.prof["filter"]["ms"] > 0
+        hot = r.prof["expand"]["launches"] + r.prof["tail"]["launches"]
+        assert hot >= 1 and r.prof["expand"]["ms"] + r.prof["tail"]["ms"] > 0
+        assert r.prof["expand"]["alg_bytes"] + r.prof["tail"]["alg_bytes"] > 0 and r.prof["filter"]["ms"] > 0
         rt = run(G, gi.query("K3"), "enumerate")[1]
         re = gsm.gsm_match(G, 3, gi.query("K3").edges, mode=gsm.GSM_MODE_ENUMERATE)
         t = re.rows_torch()

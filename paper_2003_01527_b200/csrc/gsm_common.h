@@ -54,6 +54,13 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define GSM_CUDA(call) ::gsm::cuda_check((call), #call, __FILE__, __LINE__)
 #define GSM_LAUNCH(what) ::gsm::cuda_check(cudaGetLastError(), what, __FILE__, __LINE__)
 
+// ---------------------------------------------------------------- host-side trace (GSM_TRACE=1)
+struct HostTrace {
+    double alloc_ms = 0, alloc_bytes = 0, sync_ms = 0;
+    long allocs = 0, syncs = 0;
+};
+extern HostTrace g_trace;
+
 // ---------------------------------------------------------------- device memory
 // Stream-ordered allocations from the device's default memory pool.
 void* dev_alloc(size_t bytes, cudaStream_t s);

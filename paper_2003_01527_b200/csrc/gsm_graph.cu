@@ -12,6 +12,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -32,9 +33,15 @@ static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 void clear_error() { g_last_error.clear(); }
 
+HostTrace g_trace;
+
 void* dev_alloc(size_t bytes, cudaStream_t s) {
     void* p = nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    g_trace.alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    g_trace.allocs++;
+    g_trace.alloc_bytes += (double)bytes;
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
         char buf[160];

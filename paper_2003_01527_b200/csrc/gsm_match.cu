@@ -86,8 +86,11 @@ struct LevelBufs {
 template <typename T>
 T read_scalar(const T* dptr, cudaStream_t s) {
     T h{};
+    const auto t0 = Clock::now();
     GSM_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
     GSM_CUDA(cudaStreamSynchronize(s));
+    g_trace.sync_ms += ms_since(t0);
+    g_trace.syncs++;
     return h;
 }
 
@@ -536,6 +539,7 @@ void match_impl(const gsm_graph* gh, const gsm_query* q, const gsm_match_opts* u
     if (!opts.root_subset) opts.root_subset_len = 0;
 
     const auto t0 = Clock::now();
+    g_trace = HostTrace();
     QueryPlan plan;
     std::string msg;
     gsm_status st = load_query(q, &plan, &msg);
@@ -567,6 +571,16 @@ void match_impl(const gsm_graph* gh, const gsm_query* q, const gsm_match_opts* u
     }
     out->ms_plan = plan_ms;
     out->ms_total += plan_ms;
+    if (const char* tr = getenv("GSM_TRACE")) {
+        if (tr[0] == '1')
+            std::fprintf(stderr,
+                         "[gsm] k=%d count=%llu total %.1f ms (filter %.1f expand %.1f finalize %.1f) | allocs %ld "
+                         "(%.2f GB, %.1f ms) syncs %ld (%.1f ms, includes kernel waits) chunks %llu\n",
+                         plan.k, (unsigned long long)out->count, out->ms_total, out->ms_filter, out->ms_expand,
+                         out->ms_finalize, g_trace.allocs, g_trace.alloc_bytes / 1e9, g_trace.alloc_ms,
+                         g_trace.syncs, g_trace.sync_ms, (unsigned long long)out->num_chunks);
+    }
+    g_trace = HostTrace();
     cudaSetDevice(prev);
 }
 

@@ -907,7 +907,36 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             n += __popc(ball);
         }
         __syncwarp();
-        // ---- phase 2: pairs (c, d) inside RC(r)
+        // ---- phase 2a: small RC with d ≻ c: the n(n-1)/2 pairs (c, d) = (RC[i], RC[j]), i < j,
+        //      spread over the lanes (one independent search of d in N+(c) per lane)
+        if (a.rel > 0 && !Lc.keyed && n <= 64) {
+            const int np = n * (n - 1) / 2;
+            for (int pidx = lane; pidx < np; pidx += 32) {
+                const float fn = 2.0f * n - 1.0f;
+                int i = (int)((fn - sqrtf(fn * fn - 8.0f * pidx)) * 0.5f);
+                i = max(0, min(i, n - 2));
+                while (i > 0 && i * (2 * n - i - 1) / 2 > pidx) --i;
+                while ((i + 1) * (2 * n - i - 2) / 2 <= pidx) ++i;
+                const int j = pidx - i * (2 * n - i - 1) / 2 + i + 1;
+                const int32_t c = rc[i], d = rc[j];
+                ++items;
+                bool ok = true;
+                if (Lc.check_mask) ok = (cmask[c] >> Lc.qv) & 1u;
+                for (int q = 0; q < Lc.ninj && ok; ++q) ok = c != row[Lc.inj[q]];
+                if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                if (ok) {
+                    const int64_t s0 = a.off[c] + a.up[c], t0 = a.off[c + 1];
+                    ok = in_sorted(cols + s0, (int)(t0 - s0), d, probes);
+                }
+                cnt += ok;
+            }
+            __syncwarp();
+            continue;
+        }
+        // ---- phase 2b: pairs (c, d) inside RC(r), one c at a time across the warp
         for (int i = 0; i < n; ++i) {
             const int32_t c = rc[i];
             bool okc = true;
@@ -919,8 +948,15 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             else if (a.rel < 0) j1 = i;
             if (j1 <= j0) continue;
             const int64_t cs = a.off[c], ce = a.off[c + 1];
-            const int64_t s0 = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rc[j0]));
-            const int64_t t0 = lower_bound_cols(cols, s0, ce, (int64_t)(kb | rc[j1 - 1]) + 1);
+            int64_t s0, t0;
+            if (!Lc.keyed && a.rel != 0) {  // d ≻ c (or ≺ c): exactly N+(c) (or N-(c)) via up[c], no search
+                const int64_t split = cs + a.up[c];
+                s0 = a.rel > 0 ? split : cs;
+                t0 = a.rel > 0 ? ce : split;
+            } else {
+                s0 = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rc[j0]));
+                t0 = lower_bound_cols(cols, s0, ce, (int64_t)(kb | rc[j1 - 1]) + 1);
+            }
             const int64_t nA = j1 - j0, nB = t0 - s0;
             if (nB <= 0) continue;
             if (nA <= nB) {
@@ -1034,8 +1070,15 @@ __global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan L
             else if (a.rel < 0) j1 = i;
             if (j1 <= j0) continue;
             const int64_t cs = a.off[c], ce = a.off[c + 1];
-            const int64_t s0 = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rcb[j0]));
-            const int64_t t0 = lower_bound_cols(cols, s0, ce, (int64_t)(kb | rcb[j1 - 1]) + 1);
+            int64_t s0, t0;
+            if (!Lc.keyed && a.rel != 0) {
+                const int64_t split = cs + a.up[c];
+                s0 = a.rel > 0 ? split : cs;
+                t0 = a.rel > 0 ? ce : split;
+            } else {
+                s0 = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rcb[j0]));
+                t0 = lower_bound_cols(cols, s0, ce, (int64_t)(kb | rcb[j1 - 1]) + 1);
+            }
             const int64_t nA = j1 - j0, nB = t0 - s0;
             if (nB <= 0) continue;
             if (nA <= nB) {

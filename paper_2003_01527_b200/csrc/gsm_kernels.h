@@ -83,6 +83,7 @@ struct TailArgs {
     const int64_t* cbeg;
     const int32_t* clen;
     const int64_t* off;
+    const int32_t* up;      // plain lists: N+(v) starts at off[v] + up[v]
     const int32_t* cols;    // plain or keyed lists (same as position k-2's)
     const void* cmask;
     int32_t rel;            // +1: f(π[k-1]) ≻ f(π[k-2]); -1: ≺; 0: unconstrained

@@ -348,6 +348,7 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
     a.cbeg = B.cbeg.p;
     a.clen = B.clen.p;
     a.off = g_.off;
+    a.up = g_.up;
     a.cols = L.keyed ? g_.lkeys : g_.cols;
     a.cmask = cmask_.p;
     a.cap = tail_cap();

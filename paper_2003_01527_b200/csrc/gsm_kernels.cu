@@ -648,7 +648,7 @@ bool use_walk(const LevelPlan& L) {
 }
 
 int64_t expand_tile_for(const LevelPlan& L) {
-    return use_walk(L) ? (int64_t)kThreads * kWalkVT : expand_tile(L.width);
+    return use_walk(L) ? (int64_t)32 * kWalkVT : expand_tile(L.width);
 }
 
 // first index in [p, e) with a[idx] >= key, galloping from p
@@ -676,25 +676,31 @@ __device__ __forceinline__ int64_t gallop(const int32_t* __restrict__ a, int64_t
 
 template <typename MaskT>
 __global__ void __launch_bounds__(kThreads) k_count_walk(ExpandArgs a, LevelPlan L) {
-    extern __shared__ __align__(16) int64_t sA[];  // row ends P[r+1] of the tile's rows
+    // warp-private tiles (TD = 32 * kWalkVT merge steps): no block barriers, so a lane
+    // with a long walk only delays its own warp
+    extern __shared__ __align__(16) int64_t sAall[];
     const int64_t TD = a.TD;
-    const int W = L.width;
+    const int lane_id = threadIdx.x & 31;
+    int64_t* sA = sAall + (threadIdx.x >> 5) * (TD + 1);  // row ends P[r+1] of the tile's rows
     const int nb = L.nb;
+    const int W = L.width;
     const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
     const int32_t* __restrict__ cols = a.cols;
     unsigned long long cnt = 0;
     unsigned st_items = 0, st_mask = 0, st_probes = 0, st_lists = 0;
-    for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = gw; t < a.ntiles; t += nw) {
         const int64_t d0 = a.D0 + t * TD;
         const int64_t d1 = min(d0 + TD, a.D1);
         const int64_t ra0 = a.tile_ra[t], ra1 = a.tile_ra[t + 1];
-        if (d1 - ra1 <= d0 - ra0) continue;  // no candidates in this tile (block-uniform)
+        if (d1 - ra1 <= d0 - ra0) continue;  // no candidates in this tile (warp-uniform)
         const int64_t rlast = min(ra1, a.R - 1);
         const int nrows = (int)(rlast - ra0 + 1);
-        __syncthreads();
-        for (int i = threadIdx.x; i < nrows; i += kThreads) sA[i] = a.P[ra0 + i + 1];
-        __syncthreads();
-        const int64_t d = d0 + (int64_t)threadIdx.x * kWalkVT;
+        __syncwarp();
+        for (int i = lane_id; i < nrows; i += 32) sA[i] = a.P[ra0 + i + 1];
+        __syncwarp();
+        const int64_t d = d0 + (int64_t)lane_id * kWalkVT;
         if (d >= d1) continue;
         // merge-path split for diagonal d inside [ra0, ra1]
         int64_t lo = ra0, hi = min(ra1, d);
@@ -779,13 +785,14 @@ __global__ void __launch_bounds__(kThreads) k_count_walk(ExpandArgs a, LevelPlan
 
 template <typename MaskT>
 static void launch_walk_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
-    const size_t smem = sizeof(int64_t) * (size_t)(a.TD + 1);
+    const size_t smem = sizeof(int64_t) * (size_t)(a.TD + 1) * kWarps;
     GSM_CUDA(cudaFuncSetAttribute(k_count_walk<MaskT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     int dev = 0, sms = 148, per_sm = 1;
     GSM_CUDA(cudaGetDevice(&dev));
     GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_walk<MaskT>, kThreads, smem));
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(a.ntiles, (int64_t)sms * std::max(per_sm, 1)));
+    const int64_t grid =
+        std::max<int64_t>(1, std::min<int64_t>((a.ntiles + kWarps - 1) / kWarps, (int64_t)sms * std::max(per_sm, 1)));
     k_count_walk<MaskT><<<(unsigned)grid, kThreads, smem, s>>>(a, L);
     GSM_LAUNCH("k_count_walk");
 }
@@ -834,7 +841,7 @@ static void launch_expand_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_
 }
 
 void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cudaStream_t s) {
-    if (use_walk(L) && a.TD == (int64_t)kThreads * kWalkVT) {
+    if (use_walk(L) && a.TD == (int64_t)32 * kWalkVT) {
         switch (mask_bytes) {
             case 1: launch_walk_t<uint8_t>(a, L, s); break;
             case 2: launch_walk_t<uint16_t>(a, L, s); break;

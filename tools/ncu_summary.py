@@ -113,7 +113,53 @@ def launches(csvpath, outmd):
     print("\n".join(lines))
 
 
+def metrics(csvpath, workload):
+    """Per-kernel mean DRAM bytes / duration per launch from an `ncu --metrics ... --csv` log;
+    merged into profiles/ncu_summary.json under <workload> (bench.py reads `traffic`)."""
+    txt = open(csvpath).read()
+    start = txt.find('"ID"')
+    rd = list(csv.reader(io.StringIO(txt[start:])))
+    header, rows = rd[0], rd[1:]
+    idx = {h: i for i, h in enumerate(header)}
+    per = defaultdict(lambda: defaultdict(list))
+    for r in rows:
+        if len(r) < len(header):
+            continue
+        name = r[idx["Kernel Name"]].split("(")[0].split("<")[0].strip()
+        m = r[idx["Metric Name"]]
+        v = to_float(r[idx["Metric Value"]])
+        u = r[idx["Metric Unit"]]
+        if v is None:
+            continue
+        if m.startswith("dram__bytes"):
+            v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
+        if m == "gpu__time_duration.sum":
+            v *= {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(u, 1e-9)
+        per[name][m].append(v)
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        allp = json.load(open(path))
+    except (OSError, ValueError):
+        allp = {}
+    summ = allp.get(workload, {})
+    for name, ms in per.items():
+        n = max(len(v) for v in ms.values())
+        rd_ = sum(ms.get("dram__bytes_read.sum", [0])) / n
+        wr_ = sum(ms.get("dram__bytes_write.sum", [0])) / n
+        dur = sum(ms.get("gpu__time_duration.sum", [0])) / n
+        e = summ.setdefault(name, {})
+        e.update({"launches_measured": n, "dram_read_per_launch": rd_, "dram_write_per_launch": wr_,
+                  "dram_bytes_per_launch": rd_ + wr_, "duration_s_per_launch_ncu": dur,
+                  "source": os.path.basename(csvpath)})
+    allp[workload] = summ
+    json.dump(allp, open(path, "w"), indent=1, sort_keys=True)
+    print(json.dumps(summ, indent=1))
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "metrics":
+        metrics(sys.argv[2], sys.argv[3])
+        sys.exit(0)
     if sys.argv[1] == "full":
         full(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else None)
     else:

@@ -18,9 +18,11 @@
 #include <new>
 
 #include "gsm_common.h"
+#include "gsm_workspace.h"
 
 struct gsm_graph {
     gsm::DevGraph g;
+    std::unique_ptr<gsm::Workspace> ws{new gsm::Workspace()};
     int device = 0;
     cudaStream_t stream = 0;
     bool own_stream = false;
@@ -192,6 +194,8 @@ static void free_graph(gsm_graph* h) {
     cudaGetDevice(&cur);
     cudaSetDevice(h->device);
     DevGraph& g = h->g;
+    cudaStreamSynchronize(h->stream);
+    h->ws.reset();  // frees the cached match workspace (stream-ordered)
     cudaStreamSynchronize(h->stream);
     cudaFree(g.off);
     cudaFree(g.cols);
@@ -438,4 +442,5 @@ const DevGraph& graph_of(const gsm_graph* h) { return h->g; }
 int device_of(const gsm_graph* h) { return h->device; }
 cudaStream_t stream_of(const gsm_graph* h) { return h->stream; }
 bool labeled_of(const gsm_graph* h) { return h->labeled; }
+Workspace& workspace_of(const gsm_graph* h) { return *h->ws; }
 }  // namespace gsm

@@ -20,6 +20,7 @@
 
 #include "gsm_common.h"
 #include "gsm_kernels.h"
+#include "gsm_workspace.h"
 
 namespace gsm {
 
@@ -27,6 +28,7 @@ const DevGraph& graph_of(const gsm_graph* h);
 int device_of(const gsm_graph* h);
 cudaStream_t stream_of(const gsm_graph* h);
 bool labeled_of(const gsm_graph* h);
+Workspace& workspace_of(const gsm_graph* h);
 
 namespace {
 
@@ -72,17 +74,6 @@ struct Recorder {
     }
 };
 
-struct LevelBufs {
-    DevBuf<int32_t> rows;  // frontier of this width (input rows of process(width))
-    int64_t cap_rows = 0;  // row capacity reserved for this frontier (0 = unbounded roots)
-    DevBuf<int64_t> rbeg, rlen, P, tile_ra, cbeg;
-    DevBuf<int32_t> clen;
-    DevBuf<uint8_t> rpiv, scan_tmp;
-    DevBuf<unsigned long long> out_count;
-    unsigned long long* stats = nullptr;  // 5 counters for this width's expand launches
-    double rows_in = 0;                   // rows staged by this width's expand launches
-};
-
 template <typename T>
 T read_scalar(const T* dptr, cudaStream_t s) {
     T h{};
@@ -97,7 +88,9 @@ T read_scalar(const T* dptr, cudaStream_t s) {
 class Matcher {
    public:
     Matcher(const gsm_graph* gh, QueryPlan& plan, const gsm_match_opts& o, gsm_result* res, cudaStream_t s)
-        : g_(graph_of(gh)), plan_(plan), opts_(o), res_(res), s_(s) {
+        : g_(graph_of(gh)), plan_(plan), opts_(o), res_(res), s_(s), ws_(workspace_of(gh)), lv_(ws_.lv),
+          cmask_(ws_.cmask), final_count_(ws_.final_count), stats_(ws_.stats), ovf_idx_(ws_.ovf_idx),
+          ovf_rows_(ws_.ovf_rows), ovf_n_(ws_.ovf_n) {
         rec_.prof = (o.flags & GSM_FLAG_PROFILE) != 0;
         rec_.s = s;
         rec_.res = res;
@@ -120,14 +113,18 @@ class Matcher {
     cudaStream_t s_;
     Recorder rec_;
 
+    Workspace& ws_;                                 // per-graph buffers, reused across matches
+    std::vector<std::unique_ptr<LevelBufs>>& lv_;   // index = width 1..k
+    DevBuf<uint8_t>& cmask_;
+    DevBuf<unsigned long long>& final_count_;       // COUNT mode: survivors at the last level
+    DevBuf<unsigned long long>& stats_;             // 5 per width (+ tail slot)
+    DevBuf<int64_t>& ovf_idx_;
+    DevBuf<int32_t>& ovf_rows_;
+    DevBuf<unsigned long long>& ovf_n_;
     int k_ = 0;
     int mask_bytes_ = 1;
     bool count_mode_ = true;
-    DevBuf<uint8_t> cmask_;
     std::vector<LevelPlan> lplan_;
-    std::vector<std::unique_ptr<LevelBufs>> lv_;  // index = width 1..k
-    DevBuf<unsigned long long> final_count_;      // COUNT mode: survivors at the last level
-    DevBuf<unsigned long long> stats_;            // 5 per width
     DevBuf<int32_t> arena_;                       // ENUMERATE: rows in position order, new ids
     int64_t arena_rows_ = 0;
     int64_t budget_ = 0;
@@ -135,9 +132,6 @@ class Matcher {
     bool tail_ = false;        // fuse the last two positions (COUNT mode)
     TailArgs tail_args_;
     double tail_rows_ = 0;     // rows handled by the fused tail
-    DevBuf<int64_t> ovf_idx_;
-    DevBuf<int32_t> ovf_rows_;
-    DevBuf<unsigned long long> ovf_n_;
 };
 
 void Matcher::run() {
@@ -157,7 +151,7 @@ void Matcher::run() {
         fq.qdeg[u] = plan_.qdeg[u];
     }
     cmask_.ensure((size_t)g_.n * mask_bytes_, s_);
-    DevBuf<unsigned long long> counts;
+    DevBuf<unsigned long long>& counts = ws_.counts;
     counts.ensure(kMaxK, s_);
     GSM_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * kMaxK, s_));
     rec_.run(GSM_K_FILTER, 1, [&] { launch_filter(g_, fq, cmask_.p, counts.p, s_); });
@@ -178,8 +172,11 @@ void Matcher::run() {
     for (int i = 0; i < k_; ++i) res_->order[i] = plan_.order[i];
     res_->num_levels = k_;
     res_->width = k_;
-    lv_.resize(k_ + 1);
-    for (int w = 0; w <= k_; ++w) lv_[w].reset(new LevelBufs());
+    for (int w = 0; w <= k_; ++w) {  // reuse the graph's grow-only buffers; reset per-match state
+        lv_[w]->cap_rows = 0;
+        lv_[w]->stats = nullptr;
+        lv_[w]->rows_in = 0;
+    }
     lplan_.resize(k_);
     for (int i = 1; i < k_; ++i) {
         LevelPlan& L = lplan_[i];
@@ -231,7 +228,18 @@ void Matcher::run() {
 
     size_t free_b = 0, total_b = 0;
     GSM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    budget_ = opts_.mem_budget_bytes ? (int64_t)opts_.mem_budget_bytes : (int64_t)(free_b / 4);
+    {   // memory the stream-ordered pool holds (this graph's cached workspace included) is
+        // reusable, so the default budget stays stable across calls: min(total/4, 0.9 x available)
+        int dev = 0;
+        GSM_CUDA(cudaGetDevice(&dev));
+        cudaMemPool_t pool;
+        GSM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t reserved = 0;
+        GSM_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+        const double avail = 0.9 * ((double)free_b + (double)reserved);
+        budget_ = opts_.mem_budget_bytes ? (int64_t)opts_.mem_budget_bytes
+                                         : (int64_t)std::min((double)total_b / 4.0, avail);
+    }
     // per-width share of the budget for frontiers of width 2..k (k only when enumerating)
     const int nfront = count_mode_ ? std::max(0, k_ - 2) : k_ - 1;
     for (int w = 2; w <= k_; ++w) {
@@ -352,6 +360,7 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
     a.cols = L.keyed ? g_.lkeys : g_.cols;
     a.cmask = cmask_.p;
     a.cap = tail_cap();
+    a.bratio = tail_bratio();
     a.count = final_count_.p;
     a.overflow = ovf_idx_.p;
     a.noverflow = ovf_n_.p;

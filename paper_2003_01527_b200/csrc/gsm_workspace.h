@@ -1,0 +1,35 @@
+// gsm_workspace.h — per-graph device workspace reused across gsm_match calls
+// (grow-only buffers: frontiers, per-row plans, counters), so steady-state
+// matches do no device allocation.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "gsm_common.h"
+
+namespace gsm {
+
+struct LevelBufs {
+    DevBuf<int32_t> rows;  // frontier of this width (input rows of process(width))
+    int64_t cap_rows = 0;  // row capacity reserved for this frontier (per match)
+    DevBuf<int64_t> rbeg, rlen, P, tile_ra, cbeg;
+    DevBuf<int32_t> clen;
+    DevBuf<uint8_t> rpiv, scan_tmp;
+    DevBuf<unsigned long long> out_count;
+    unsigned long long* stats = nullptr;  // 5 counters for this width's expand launches (per match)
+    double rows_in = 0;                   // rows staged by this width's expand launches (per match)
+};
+
+struct Workspace {
+    std::vector<std::unique_ptr<LevelBufs>> lv;  // index = frontier width 1..k
+    DevBuf<uint8_t> cmask;
+    DevBuf<unsigned long long> counts, final_count, stats, ovf_n;
+    DevBuf<int64_t> ovf_idx;
+    DevBuf<int32_t> ovf_rows;
+    Workspace() : lv(kMaxK + 1) {
+        for (auto& p : lv) p.reset(new LevelBufs());
+    }
+};
+
+}  // namespace gsm

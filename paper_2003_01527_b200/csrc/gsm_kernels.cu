@@ -873,8 +873,8 @@ void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cuda
 // Rows whose pivot segment exceeds the per-warp buffer are handed back (overflow
 // list) to the generic BFS path.
 // ============================================================================
-// per-warp shared memory of k_tail: RC[cap] + item offsets[cap+1] + strategy bytes[cap]
-__host__ __device__ inline int tail_warp_ints(int cap) { return cap + (cap + 1) + (cap + 3) / 4 + 1; }
+// per-warp shared memory of k_tail: RC[cap]
+__host__ __device__ inline int tail_warp_ints(int cap) { return cap; }
 
 template <typename MaskT>
 __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, LevelPlan Ld) {
@@ -917,65 +917,30 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             n += __popc(ball);
         }
         __syncwarp();
-        // ---- phase 2a (d ≻ c, plain lists): load-balanced over the lanes.  For every c = RC[i]
-        //      pick the cheaper side — A: search each later RC entry in N+(c) (global binary
-        //      search), or B: stream N+(c) and search each entry in RC (shared memory) — then
-        //      spread all (c, item) pairs of the row over the 32 lanes via a warp prefix sum.
-        if (a.rel > 0 && !Lc.keyed) {
-            int32_t* pre = rc + a.cap;                 // [n+1] item offsets
-            uint8_t* useB = reinterpret_cast<uint8_t*>(pre + a.cap + 1);  // [n] strategy
-            int carry = 0;
-            for (int base = 0; base < n; base += 32) {
-                const int i = base + lane;
-                int it = 0;
-                if (i < n) {
-                    const int32_t c = rc[i];
-                    bool okc = true;
-                    if (Lc.check_mask) okc = (cmask[c] >> Lc.qv) & 1u;
-                    for (int q = 0; q < Lc.ninj && okc; ++q) okc = c != row[Lc.inj[q]];
-                    const int nA = n - 1 - i;
-                    const int lenB = okc && nA > 0 ? (int)(a.off[c + 1] - a.off[c] - a.up[c]) : 0;
-                    const bool b = lenB <= a.bratio * nA;
-                    it = (!okc || nA <= 0 || lenB <= 0) ? 0 : (b ? lenB : nA);
-                    useB[i] = b ? 1 : 0;
-                }
-                int incl = it;  // warp inclusive scan
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                if (i < n) pre[i] = carry + incl - it;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            if (lane == 0) pre[n] = carry;
-            __syncwarp();
-            const int total = carry;
-            for (int pidx = lane; pidx < total; pidx += 32) {
-                int lo = 0, hi = n;  // largest i with pre[i] <= pidx
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (pre[mid] <= pidx) lo = mid + 1; else hi = mid;
-                }
-                const int i = lo - 1;
-                const int e = pidx - pre[i];
-                const int32_t c = rc[i];
-                const int64_t s0 = a.off[c] + a.up[c], t0 = a.off[c + 1];
+        // ---- phase 2a: small RC with d ≻ c: the n(n-1)/2 pairs (c, d) = (RC[i], RC[j]), i < j,
+        //      spread over the lanes (one independent search of d in N+(c) per lane)
+        if (a.rel > 0 && !Lc.keyed && n <= 64) {
+            const int np = n * (n - 1) / 2;
+            for (int pidx = lane; pidx < np; pidx += 32) {
+                const float fn = 2.0f * n - 1.0f;
+                int i = (int)((fn - sqrtf(fn * fn - 8.0f * pidx)) * 0.5f);
+                i = max(0, min(i, n - 2));
+                while (i > 0 && i * (2 * n - i - 1) / 2 > pidx) --i;
+                while ((i + 1) * (2 * n - i - 2) / 2 <= pidx) ++i;
+                const int j = pidx - i * (2 * n - i - 1) / 2 + i + 1;
+                const int32_t c = rc[i], d = rc[j];
                 ++items;
-                int32_t d;
-                bool ok;
-                if (useB[i]) {
-                    d = cols[s0 + e];
-                    unsigned dummy = 0;
-                    ok = in_sorted(rc + i + 1, n - 1 - i, d, dummy);
-                } else {
-                    d = rc[i + 1 + e];
-                    ok = true;
-                }
+                bool ok = true;
+                if (Lc.check_mask) ok = (cmask[c] >> Lc.qv) & 1u;
+                for (int q = 0; q < Lc.ninj && ok; ++q) ok = c != row[Lc.inj[q]];
                 if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
                 for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
                 for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
                 for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
-                if (ok && !useB[i]) ok = in_sorted(cols + s0, (int)(t0 - s0), d, probes);
+                if (ok) {
+                    const int64_t s0 = a.off[c] + a.up[c], t0 = a.off[c + 1];
+                    ok = in_sorted(cols + s0, (int)(t0 - s0), d, probes);
+                }
                 cnt += ok;
             }
             __syncwarp();

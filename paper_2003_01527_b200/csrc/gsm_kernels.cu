@@ -81,6 +81,95 @@ void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigne
 }
 
 // ============================================================================
+// K5 neighbourhood-encoding refinement — Alg. 1 line 7 "Advance+Compute: NE for
+// each node in G" and line 8 "Filter ... update G's (NE, deg)" (P:108-110,
+// P:134).  NE(v) = sum of the labels of v's neighbours (each label counted as
+// label+1 so that it is positive; unlabeled: 1 per neighbour, i.e.
+// the degree), taken — like the effective degree — over the neighbours
+// that are still a candidate of some query vertex (cmask != 0), so each round
+// prunes against the previous round's survivors.  Bit u of cmask[v] survives iff
+// deg_eff(v) >= deg_Q(u) and NE(v) >= NE_Q(u).  Sound: an embedding's images
+// keep their bits (the images of u's query neighbours are distinct alive
+// neighbours of f(u) with the query's labels).  Warp per vertex over its list.
+// ============================================================================
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_refine(const int64_t* __restrict__ off,
+                                                     const int32_t* __restrict__ cols,
+                                                     const uint32_t* __restrict__ labels, int64_t n, FilterQuery q,
+                                                     const int64_t* __restrict__ qne, const MaskT* __restrict__ in,
+                                                     MaskT* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = warp; v < n; v += nwarps) {
+        const uint32_t m = in[v];
+        if (m == 0) {
+            if (lane == 0) out[v] = 0;
+            continue;
+        }
+        int64_t deg = 0, ne = 0;
+        for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+            const int32_t w = cols[e];
+            if (in[w] != 0) {
+                ++deg;
+                ne += (labels && q.use_labels) ? (int64_t)labels[w] + 1 : 1;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            deg += __shfl_xor_sync(0xffffffffu, deg, o);
+            ne += __shfl_xor_sync(0xffffffffu, ne, o);
+        }
+        if (lane == 0) {
+            uint32_t keep = m;
+            for (int u = 0; u < q.k; ++u)
+                if (((m >> u) & 1u) && (deg < q.qdeg[u] || ne < qne[u])) keep &= ~(1u << u);
+            out[v] = (MaskT)keep;
+        }
+    }
+}
+
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_mask_counts(const MaskT* __restrict__ cmask, int64_t n, int k,
+                                                          unsigned long long* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long mine = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int64_t v = base + threadIdx.x;
+        const uint32_t m = v < n ? (uint32_t)cmask[v] : 0u;
+        for (int u = 0; u < k; ++u) {
+            const unsigned b = __ballot_sync(0xffffffffu, (m >> u) & 1u);
+            if (lane == u) mine += __popc(b);
+        }
+    }
+    if (lane < k && mine) atomicAdd(&counts[lane], mine);
+}
+
+template <typename MaskT>
+static void refine_t(const DevGraph& g, const FilterQuery& q, const int64_t* qne, int rounds, void* cmask, void* tmp,
+                     unsigned long long* counts, cudaStream_t s) {
+    MaskT* a = static_cast<MaskT*>(cmask);
+    MaskT* b = static_cast<MaskT*>(tmp);
+    for (int r = 0; r < rounds; ++r) {
+        k_refine<MaskT><<<grid_for(g.n * 32), kThreads, 0, s>>>(g.off, g.cols, g.labels, g.n, q, qne, a, b);
+        GSM_LAUNCH("k_refine");
+        GSM_CUDA(cudaMemcpyAsync(a, b, sizeof(MaskT) * g.n, cudaMemcpyDeviceToDevice, s));
+    }
+    GSM_CUDA(cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * kMaxK, s));
+    k_mask_counts<MaskT><<<grid_for(g.n), kThreads, 0, s>>>(a, g.n, q.k, counts);
+    GSM_LAUNCH("k_mask_counts");
+}
+
+void launch_refine(const DevGraph& g, const FilterQuery& q, const int64_t* qne, int rounds, void* cmask, void* tmp,
+                   unsigned long long* counts, cudaStream_t s) {
+    switch (mask_bytes_for(q.k)) {
+        case 1: refine_t<uint8_t>(g, q, qne, rounds, cmask, tmp, counts, s); break;
+        case 2: refine_t<uint16_t>(g, q, qne, rounds, cmask, tmp, counts, s); break;
+        default: refine_t<uint32_t>(g, q, qne, rounds, cmask, tmp, counts, s); break;
+    }
+}
+
+// ============================================================================
 // Roots: level-0 frontier = C(π[0]) (Alg. 1 line 11: "All-source BFS traversal
 // from c_set"), compacted in ascending (degree, id) rank; multi-GPU shards keep
 // every P-th root.  Stable two-pass block-scan compaction.

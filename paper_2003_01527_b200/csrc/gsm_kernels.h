@@ -23,6 +23,11 @@ inline int mask_bytes_for(int k) { return k <= 8 ? 1 : (k <= 16 ? 2 : 4); }
 void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigned long long* counts,
                    cudaStream_t s);
 
+// K5 NE refinement (Alg. 1 lines 7-8): `rounds` passes of NE / effective-degree pruning of
+// cmask (qne: device int64[k] query NE), then counts[u] = |C(u)| recomputed.  tmp: n mask words.
+void launch_refine(const DevGraph& g, const FilterQuery& q, const int64_t* qne, int rounds, void* cmask, void* tmp,
+                   unsigned long long* counts, cudaStream_t s);
+
 // Roots: stable compaction of {v : bit `bit` of cmask[v]} in ascending new id, keeping global
 // rank r with r % nshards == shard (written at r / nshards).  Returns the number written.
 int64_t launch_roots(const DevGraph& g, const void* cmask, int mask_bytes, int bit, int shard, int nshards,

@@ -157,6 +157,22 @@ void Matcher::run() {
     rec_.run(GSM_K_FILTER, 1, [&] { launch_filter(g_, fq, cmask_.p, counts.p, s_); });
     res_->prof[GSM_K_FILTER].alg_bytes +=
         (double)g_.n * (8.0 + (plan_.use_labels ? 4.0 : 0.0) + mask_bytes_);
+    if (opts_.refine_rounds > 0) {  // Alg. 1 lines 7-8: NE filter + refinement rounds
+        int64_t hqne[kMaxK] = {};
+        for (int u = 0; u < k_; ++u)
+            for (int w = 0; w < k_; ++w)
+                if ((plan_.adj[u] >> w) & 1u) hqne[u] += plan_.use_labels ? (int64_t)plan_.qlabel[w] + 1 : 1;
+        DevBuf<int64_t> dqne;
+        DevBuf<uint8_t> tmp;
+        dqne.ensure(kMaxK, s_);
+        tmp.ensure((size_t)g_.n * mask_bytes_, s_);
+        GSM_CUDA(cudaMemcpyAsync(dqne.p, hqne, sizeof(hqne), cudaMemcpyHostToDevice, s_));
+        rec_.run(GSM_K_FILTER, 2 * opts_.refine_rounds + 1,
+                 [&] { launch_refine(g_, fq, dqne.p, opts_.refine_rounds, cmask_.p, tmp.p, counts.p, s_); });
+        res_->prof[GSM_K_FILTER].alg_bytes +=
+            opts_.refine_rounds * ((double)g_.nnz * (4.0 + mask_bytes_ + (plan_.use_labels ? 4.0 : 0.0)) +
+                                   (double)g_.n * (16.0 + 3.0 * mask_bytes_)) + (double)g_.n * mask_bytes_;
+    }
     unsigned long long hc[kMaxK];
     GSM_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, s_));
     GSM_CUDA(cudaStreamSynchronize(s_));
@@ -181,11 +197,13 @@ void Matcher::run() {
     for (int i = 1; i < k_; ++i) {
         LevelPlan& L = lplan_[i];
         L = make_level_plan(plan_, i, count_mode_ && i == k_ - 1);
+        if (opts_.refine_rounds > 0) L.check_mask = 1;  // NE-refined cmask is stronger than the degree test
         if (plan_.use_labels && g_.lkeys && plan_.qlabel[L.qv] <= g_.max_label) {
             L.keyed = 1;
             L.key_base = (int32_t)(plan_.qlabel[L.qv] << g_.idbits);
             L.idmask = (int32_t)((1u << g_.idbits) - 1u);
-            L.check_mask = plan_.qdeg[L.qv] > L.nb ? 1 : 0;  // the label is implied by the key range
+            // the label is implied by the key range; the degree by |B(i)| unless NE-refined
+            L.check_mask = (opts_.refine_rounds > 0 || plan_.qdeg[L.qv] > L.nb) ? 1 : 0;
         }
     }
 
@@ -544,6 +562,7 @@ void match_impl(const gsm_graph* gh, const gsm_query* q, const gsm_match_opts* u
     if (opts.mode != GSM_MODE_COUNT && opts.mode != GSM_MODE_ENUMERATE) fail(GSM_ERR_INVALID_ARGUMENT, "bad mode");
     if (opts.num_shards > 1 && (opts.shard_index < 0 || opts.shard_index >= opts.num_shards))
         fail(GSM_ERR_INVALID_ARGUMENT, "shard_index out of range");
+    if (opts.refine_rounds < 0 || opts.refine_rounds > 64) fail(GSM_ERR_INVALID_ARGUMENT, "refine_rounds out of range");
     if (opts.root_subset_len < 0 || (opts.root_subset_len > 0 && !opts.root_subset))
         fail(GSM_ERR_INVALID_ARGUMENT, "bad root_subset");
     if (!opts.root_subset) opts.root_subset_len = 0;

@@ -48,7 +48,7 @@ class gsm_query(ctypes.Structure):
 
 class gsm_match_opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("mode", ctypes.c_int32), ("flags", ctypes.c_uint32),
-                ("shard_index", ctypes.c_int32), ("num_shards", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("shard_index", ctypes.c_int32), ("num_shards", ctypes.c_int32), ("refine_rounds", ctypes.c_int32),
                 ("root_subset", ctypes.POINTER(ctypes.c_int32)), ("root_subset_len", ctypes.c_int64),
                 ("mem_budget_bytes", ctypes.c_uint64), ("stream", ctypes.c_void_p)]
 
@@ -232,12 +232,12 @@ class Result:
 
 def gsm_match(g: Graph, num_nodes: int, edges: Sequence, labels=None, mode: int = GSM_MODE_COUNT, flags: int = 0,
               shard_index: int = 0, num_shards: int = 1, root_subset=None, mem_budget_bytes: int = 0,
-              stream: Optional[int] = None) -> Result:
+              stream: Optional[int] = None, refine_rounds: int = 0) -> Result:
     """Count (mode=GSM_MODE_COUNT) or enumerate (GSM_MODE_ENUMERATE) the embeddings of the
     query (num_nodes, edges, labels) in g.  Rows are freed with gsm_result_free / Result.free."""
     q, keep = _query(num_nodes, edges, labels)
     rs = None if root_subset is None else np.ascontiguousarray(np.asarray(root_subset, dtype=np.int32))
-    opts = gsm_match_opts(ctypes.sizeof(gsm_match_opts), mode, flags, shard_index, num_shards, 0,
+    opts = gsm_match_opts(ctypes.sizeof(gsm_match_opts), mode, flags, shard_index, num_shards, refine_rounds,
                           None if rs is None else rs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                           0 if rs is None else len(rs), mem_budget_bytes, stream)
     r = gsm_result()

@@ -142,6 +142,32 @@ def test_fused_tail_matches_generic_path(tail, monkeypatch):
         G.free()
 
 
+def test_ne_refinement_is_sound():
+    """NE filter + refinement rounds (Alg. 1 lines 7-8): results
+    identical for R = 0..3; |C(u)| non-increasing in R and never below the number of
+    distinct images of u in the oracle's embeddings (filter soundness)."""
+    g = gi.rmat(11, 8, seed=21).with_labels(gi.uniform_labels(2048, 3, 21))
+    G = load(g)
+    try:
+        for q in [gi.query("K3"), gi.query("K4"), gi.query("house", [0, 1, 2, 0, 1]), gi.query("P4", [1, 2, 2, 1]),
+                  gi.query("C4"), gi.query("S3", [0, 1, 1, 2])]:
+            cnt, ref = oracle.match(g, q)
+            images = [len(np.unique(ref[:, u])) for u in range(q.num_nodes)]
+            prev = None
+            for R in range(4):
+                c, rows, r = run(G, q, "enumerate", refine_rounds=R)
+                assert c == cnt, (q.name, R)
+                assert_rows_equal(rows, ref, f"{q.name} R={R}")
+                assert run(G, q, "count", refine_rounds=R)[0] == cnt
+                for u in range(q.num_nodes):
+                    assert r.candidates[u] >= images[u], (q.name, R, u)
+                    if prev is not None:
+                        assert r.candidates[u] <= prev[u]
+                prev = r.candidates
+    finally:
+        G.free()
+
+
 def test_closed_forms_on_gpu():
     for n in (5, 8):
         G = load(gi.complete(n))

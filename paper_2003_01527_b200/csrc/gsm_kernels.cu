@@ -1058,7 +1058,10 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             }
             const int64_t nA = j1 - j0, nB = t0 - s0;
             if (nB <= 0) continue;
-            if (nA <= nB) {
+            // A (search RC's entries in N(c), global binary searches: ~log2(nB) dependent loads
+            // each) vs B (stream N(c) coalesced, search each entry in RC in shared memory, stop
+            // at max RC): B is ~8x cheaper per element, so A only when nB is far longer
+            if (nB > (int64_t)a.bratio * nA) {
                 for (int j = j0 + lane; j < j1; j += 32) {
                     if (j == i) continue;
                     const int32_t d = rc[j];
@@ -1072,8 +1075,12 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
                     cnt += ok;
                 }
             } else {
-                for (int64_t x = s0 + lane; x < t0; x += 32) {
-                    const int32_t d = cols[x] & idm;
+                const int32_t dmax = rc[j1 - 1];
+                for (int64_t x0 = s0; x0 < t0; x0 += 32) {
+                    const int64_t x = x0 + lane;
+                    const int32_t d = x < t0 ? (cols[x] & idm) : INT32_MAX;
+                    if (!__any_sync(0xffffffffu, d <= dmax)) break;  // N(c) is sorted: past max RC
+                    if (d > dmax) continue;
                     ++items;
                     unsigned dummy = 0;
                     bool ok = d != c && in_sorted(rc + j0, j1 - j0, d, dummy);
@@ -1180,7 +1187,10 @@ __global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan L
             }
             const int64_t nA = j1 - j0, nB = t0 - s0;
             if (nB <= 0) continue;
-            if (nA <= nB) {
+            // A (search RC's entries in N(c), global binary searches: ~log2(nB) dependent loads
+            // each) vs B (stream N(c) coalesced, search each entry in RC in shared memory, stop
+            // at max RC): B is ~8x cheaper per element, so A only when nB is far longer
+            if (nB > (int64_t)a.bratio * nA) {
                 for (int j = j0 + lane; j < j1; j += 32) {
                     if (j == i) continue;
                     const int32_t d = rcb[j];
@@ -1194,8 +1204,12 @@ __global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan L
                     cnt += ok;
                 }
             } else {
-                for (int64_t x = s0 + lane; x < t0; x += 32) {
-                    const int32_t d = cols[x] & idm;
+                const int32_t dmax = rcb[j1 - 1];
+                for (int64_t x0 = s0; x0 < t0; x0 += 32) {
+                    const int64_t x = x0 + lane;
+                    const int32_t d = x < t0 ? (cols[x] & idm) : INT32_MAX;
+                    if (!__any_sync(0xffffffffu, d <= dmax)) break;  // N(c) is sorted: past max RC
+                    if (d > dmax) continue;
                     ++items;
                     unsigned dummy = 0;
                     bool ok = d != c && in_sorted(rcb + j0, j1 - j0, d, dummy);
@@ -1255,7 +1269,7 @@ int tail_block_cap() {  // per-CTA buffer for big rows (GSM_TAIL_BLOCK_CAP)
 
 int tail_bratio() {  // phase-2 strategy: stream N+(c) (B) when |N+(c)| <= ratio x later RC entries
     const char* v = getenv("GSM_TAIL_BRATIO");
-    return (v && *v) ? atoi(v) : 4;
+    return (v && *v) ? atoi(v) : 8;
 }
 
 int tail_cap() {  // per-warp candidate buffer; GSM_TAIL_CAP (tests force the overflow path with it)

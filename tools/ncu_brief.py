@@ -18,7 +18,15 @@ src = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv"], t
 rows = list(csv.reader(src.splitlines()))
 hh = rows[1]
 iS, iE = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Instructions Executed")
-body = [x for x in rows[2:] if len(x) == len(hh)]
+def _isint(v):
+    try:
+        int(v)
+        return True
+    except ValueError:
+        return False
+
+
+body = [x for x in rows[2:] if len(x) == len(hh) and _isint(x[iS]) and _isint(x[iE])]
 tot = sum(int(x[iS]) for x in body)
 print("stall samples", tot, "instructions", sum(int(x[iE]) for x in body))
 for x in sorted(body, key=lambda x: -int(x[iS]))[:int(sys.argv[2]) if len(sys.argv) > 2 else 15]:

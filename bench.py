@@ -102,14 +102,20 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- distributed
+# GSM_BENCH_ONE_DEVICE=1: every rank uses cuda:0 and the collectives go over gloo — a
+# functional check of the multi-rank path on a single-GPU box (NCCL needs one GPU per rank);
+# never a scaling measurement.
+ONE_DEVICE = os.environ.get("GSM_BENCH_ONE_DEVICE", "0") == "1"
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if ONE_DEVICE else int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if args.impl == "ours" else "gloo"
+        backend = "nccl" if (args.impl == "ours" and not ONE_DEVICE) else "gloo"
         if backend == "nccl":
             import torch
             torch.cuda.set_device(local)
@@ -297,11 +303,12 @@ def run_ours(args, world, rank, local, dist):
     barrier()
     ms = sum(ms_steps) / len(ms_steps)
     c_all, c_uni = counts
+    cdev = "cpu" if ONE_DEVICE else dev
     if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        c = torch.tensor([c_all, c_uni, launches], dtype=torch.int64, device=dev)
+        c = torch.tensor([c_all, c_uni, launches], dtype=torch.int64, device=cdev)
         dist.all_reduce(c)
         c_all, c_uni, launches = (int(x) for x in c.tolist())
 
@@ -325,10 +332,10 @@ def run_ours(args, world, rank, local, dist):
         ev1.synchronize()
         e_ms = ev0.elapsed_time(ev1) / args.e2e_steps
         if dist is not None:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            t = torch.tensor([e_ms], dtype=torch.float64, device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-            c = torch.tensor([e_cnt], dtype=torch.int64, device=dev)
+            c = torch.tensor([e_cnt], dtype=torch.int64, device=cdev)
             dist.all_reduce(c)
             e_cnt = int(c.item())
         h2d = (g.offsets.nbytes + g.cols.nbytes + (0 if g.labels is None else g.labels.nbytes)) * world
@@ -357,6 +364,7 @@ def run_ours(args, world, rank, local, dist):
             "share_of_step": (kp["ms"] / args.steps) / ms if ms > 0 else None,
             "per_kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof_tot.items()}}
     out = {"metric": "embeddings/s", "value": c_all / (ms / 1000.0), "unit": "embeddings/s", "n_gpus": world,
+           **({"one_device_functional_check": True} if ONE_DEVICE else {}),
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
            "config": config_of(w, g),

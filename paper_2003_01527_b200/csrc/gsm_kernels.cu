@@ -1058,10 +1058,10 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             }
             const int64_t nA = j1 - j0, nB = t0 - s0;
             if (nB <= 0) continue;
-            // A (search RC's entries in N(c), global binary searches: ~log2(nB) dependent loads
-            // each) vs B (stream N(c) coalesced, search each entry in RC in shared memory, stop
-            // at max RC): B is ~8x cheaper per element, so A only when nB is far longer
-            if (nB > (int64_t)a.bratio * nA) {
+            // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
+            // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
+            // enumerate the shorter side (measured: biasing towards B is slower)
+            if (nB * 100 > (int64_t)a.bratio * nA) {
                 for (int j = j0 + lane; j < j1; j += 32) {
                     if (j == i) continue;
                     const int32_t d = rc[j];
@@ -1187,10 +1187,10 @@ __global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan L
             }
             const int64_t nA = j1 - j0, nB = t0 - s0;
             if (nB <= 0) continue;
-            // A (search RC's entries in N(c), global binary searches: ~log2(nB) dependent loads
-            // each) vs B (stream N(c) coalesced, search each entry in RC in shared memory, stop
-            // at max RC): B is ~8x cheaper per element, so A only when nB is far longer
-            if (nB > (int64_t)a.bratio * nA) {
+            // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
+            // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
+            // enumerate the shorter side (measured: biasing towards B is slower)
+            if (nB * 100 > (int64_t)a.bratio * nA) {
                 for (int j = j0 + lane; j < j1; j += 32) {
                     if (j == i) continue;
                     const int32_t d = rcb[j];
@@ -1267,9 +1267,9 @@ int tail_block_cap() {  // per-CTA buffer for big rows (GSM_TAIL_BLOCK_CAP)
     return cap;
 }
 
-int tail_bratio() {  // phase-2 strategy: stream N+(c) (B) when |N+(c)| <= ratio x later RC entries
-    const char* v = getenv("GSM_TAIL_BRATIO");
-    return (v && *v) ? atoi(v) : 8;
+int tail_bratio() {  // phase-2 strategy, in percent: stream N(c) (B) when |N(c)| <= pct/100 x |RC part|
+    const char* v = getenv("GSM_TAIL_BRATIO_PCT");
+    return (v && *v) ? atoi(v) : 100;  // measured (R-MAT-20/24): 100 beats 200, 800, 3200
 }
 
 int tail_cap() {  // per-warp candidate buffer; GSM_TAIL_CAP (tests force the overflow path with it)

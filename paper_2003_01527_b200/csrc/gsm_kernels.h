@@ -93,7 +93,7 @@ struct TailArgs {
     const void* cmask;
     int32_t rel;            // +1: f(π[k-1]) ≻ f(π[k-2]); -1: ≺; 0: unconstrained
     int32_t cap;            // per-warp candidate buffer (int32 entries)
-    int32_t bratio;         // phase-2 strategy threshold (see tail_bratio)
+    int32_t bratio;         // phase-2 strategy threshold in percent (see tail_bratio)
     int32_t nxlo, nxhi;     // extra ID bounds of π[k-1] not implied by π[k-2]'s interval
     int32_t xlo[kMaxK], xhi[kMaxK];
     unsigned long long* count;

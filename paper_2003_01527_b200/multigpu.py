@@ -19,10 +19,16 @@ from typing import Callable, Optional, Sequence
 from . import gsm
 
 
+def _host_collectives(dist) -> bool:
+    """gloo (CPU tests, single-GPU functional checks) moves tensors through host memory."""
+    return dist.get_backend() == "gloo"
+
+
 def allreduce_counts(values: Sequence[int], dist, device) -> list:
     """Sum a few non-negative integer counts over all ranks (int64 tensor all-reduce)."""
     import torch
-    t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=device)
+    dev = "cpu" if _host_collectives(dist) else device
+    t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=dev)
     dist.all_reduce(t)
     return [int(x) for x in t.tolist()]
 
@@ -30,6 +36,8 @@ def allreduce_counts(values: Sequence[int], dist, device) -> list:
 def allgather_rows(rows, dist):
     """All-gather variable-length row blocks (N_r x k int32 tensors) -> concatenation in rank order."""
     import torch
+    if _host_collectives(dist) and rows.is_cuda:
+        return allgather_rows(rows.cpu(), dist).to(rows.device)
     world = dist.get_world_size()
     k = rows.shape[1]
     n = torch.tensor([rows.shape[0]], dtype=torch.int64, device=rows.device)

@@ -1061,7 +1061,27 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
             // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
             // enumerate the shorter side (measured: biasing towards B is slower)
-            if (nB * 100 > (int64_t)a.bratio * nA) {
+            if (nA >= 64 && nB >= 64 && a.rel > 0) {
+                // C: both sides long — sorted-list intersection: each lane takes a contiguous
+                // slice of RC after c and gallops forward through N(c) (O(nA + nB) total)
+                const int per = (int)((nA + 31) / 32);
+                const int x0 = j0 + lane * per, x1 = min(j1, x0 + per);
+                if (x0 < x1) {
+                    int64_t pos = lower_bound_cols(cols, s0, t0, (int64_t)(kb | rc[x0]));
+                    for (int j = x0; j < x1 && pos < t0; ++j) {
+                        const int32_t d = rc[j];
+                        ++items;
+                        pos = gallop(cols, pos, t0, kb | d, probes);
+                        if (pos >= t0 || cols[pos] != (kb | d)) continue;
+                        bool ok = true;
+                        if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                        for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                        for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                        for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                        cnt += ok;
+                    }
+                }
+            } else if (nB * 100 > (int64_t)a.bratio * nA) {
                 for (int j = j0 + lane; j < j1; j += 32) {
                     if (j == i) continue;
                     const int32_t d = rc[j];
@@ -1190,7 +1210,27 @@ __global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan L
             // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
             // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
             // enumerate the shorter side (measured: biasing towards B is slower)
-            if (nB * 100 > (int64_t)a.bratio * nA) {
+            if (nA >= 64 && nB >= 64 && a.rel > 0) {
+                // C: both sides long — sorted-list intersection: each lane takes a contiguous
+                // slice of RC after c and gallops forward through N(c) (O(nA + nB) total)
+                const int per = (int)((nA + 31) / 32);
+                const int x0 = j0 + lane * per, x1 = min(j1, x0 + per);
+                if (x0 < x1) {
+                    int64_t pos = lower_bound_cols(cols, s0, t0, (int64_t)(kb | rcb[x0]));
+                    for (int j = x0; j < x1 && pos < t0; ++j) {
+                        const int32_t d = rcb[j];
+                        ++items;
+                        pos = gallop(cols, pos, t0, kb | d, probes);
+                        if (pos >= t0 || cols[pos] != (kb | d)) continue;
+                        bool ok = true;
+                        if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                        for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                        for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                        for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                        cnt += ok;
+                    }
+                }
+            } else if (nB * 100 > (int64_t)a.bratio * nA) {
                 for (int j = j0 + lane; j < j1; j += 32) {
                     if (j == i) continue;
                     const int32_t d = rcb[j];

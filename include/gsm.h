@@ -137,9 +137,11 @@ typedef struct {
     int32_t shard_index;      /* root-candidate shard (multi-GPU); 0 */
     int32_t num_shards;       /* 0 or 1 = all roots; P = keep roots with rank % P == shard_index */
     int32_t refine_rounds;    /* neighbourhood-encoding filter (Alg. 1 lines 7-8): 0 = label +
-                                 degree only; R >= 1 = R rounds of NE(v) >= NE_Q(u) and effective
-                                 degree, each recomputed over the surviving vertices.  Sound:
-                                 never changes the result, only the candidate sets. */
+                                 degree only; R >= 1 = R rounds of NE(v) >= NE_Q(u), effective
+                                 degree, and the 1-step look-ahead condition (every query neighbour
+                                 of u has a candidate among v's neighbours), each
+                                 recomputed over the surviving vertices.  Sound: never changes the
+                                 result, only the candidate sets. */
     const int32_t* root_subset; /* HOST, optional (test/parity sampling): only embeddings with
                                    f(query vertex 0) in the subset (original ids).  Forces the
                                    query order to start at vertex 0 and implies NO_SYMMETRY. */

@@ -81,7 +81,9 @@ void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigne
 }
 
 // ============================================================================
-// K5 neighbourhood-encoding refinement — Alg. 1 line 7 "Advance+Compute: NE for
+// K5 neighbourhood-encoding refinement (with the 1-step look-ahead condition
+// folded in: bit u of v also needs, for every query neighbour u' of u, some
+// surviving neighbour of v with bit u') — Alg. 1 line 7 "Advance+Compute: NE for
 // each node in G" and line 8 "Filter ... update G's (NE, deg)" (P:108-110,
 // P:134).  NE(v) = sum of the labels of v's neighbours (each label counted as
 // label+1 so that it is positive; unlabeled: 1 per neighbour, i.e.
@@ -108,21 +110,30 @@ __global__ void __launch_bounds__(kThreads) k_refine(const int64_t* __restrict__
             continue;
         }
         int64_t deg = 0, ne = 0;
+        uint32_t nbr = 0;  // query vertices some neighbour of v can still host
         for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
             const int32_t w = cols[e];
-            if (in[w] != 0) {
+            const uint32_t mw = in[w];
+            if (mw != 0) {
                 ++deg;
                 ne += (labels && q.use_labels) ? (int64_t)labels[w] + 1 : 1;
+                nbr |= mw;
             }
         }
         for (int o = 16; o; o >>= 1) {
             deg += __shfl_xor_sync(0xffffffffu, deg, o);
             ne += __shfl_xor_sync(0xffffffffu, ne, o);
+            nbr |= __shfl_xor_sync(0xffffffffu, nbr, o);
         }
         if (lane == 0) {
             uint32_t keep = m;
-            for (int u = 0; u < q.k; ++u)
-                if (((m >> u) & 1u) && (deg < q.qdeg[u] || ne < qne[u])) keep &= ~(1u << u);
+            for (int u = 0; u < q.k; ++u) {
+                if (!((m >> u) & 1u)) continue;
+                // NE / effective degree and the 1-step look-ahead folded into the filter
+                // (a state whose query neighbour has no candidate among v's
+                // neighbours has no consistent descendant)
+                if (deg < q.qdeg[u] || ne < qne[u] || (q.qadj[u] & ~nbr) != 0) keep &= ~(1u << u);
+            }
             out[v] = (MaskT)keep;
         }
     }

@@ -13,6 +13,7 @@ struct FilterQuery {
     int32_t use_labels;
     uint32_t qlabel[kMaxK];
     int32_t qdeg[kMaxK];
+    uint32_t qadj[kMaxK];  // query adjacency bitmasks (refinement: 1-step look-ahead)
 };
 
 // mask width: 1, 2 or 4 bytes per vertex (k <= 8, 16, 32)

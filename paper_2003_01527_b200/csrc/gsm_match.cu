@@ -149,6 +149,7 @@ void Matcher::run() {
     for (int u = 0; u < k_; ++u) {
         fq.qlabel[u] = plan_.qlabel[u];
         fq.qdeg[u] = plan_.qdeg[u];
+        fq.qadj[u] = plan_.adj[u];
     }
     cmask_.ensure((size_t)g_.n * mask_bytes_, s_);
     DevBuf<unsigned long long>& counts = ws_.counts;

@@ -205,6 +205,71 @@ def uniform_labels(n: int, num_labels: int, seed: int = 1) -> np.ndarray:
     return out
 
 
+def zipf_labels(n: int, num_labels: int, seed: int = 1, alpha_num: int = 1, alpha_den: int = 1) -> np.ndarray:
+    """Power-law node labels (SPEC assign_powerlaw_labels S:54-62; "seeds the data
+    graph with power-law-distributed node ... labels"): label l in [0, L) with probability
+    proportional to (l+1)^-alpha (alpha = 1 by default).  The CDF is quantised to
+    32-bit integer thresholds so every caller draws identical labels."""
+    if num_labels < 1:
+        raise ValueError("num_labels must be >= 1")
+    alpha = alpha_num / alpha_den
+    w = np.array([(l + 1) ** (-alpha) for l in range(num_labels)], dtype=np.float64)
+    cdf = np.cumsum(w) / w.sum()
+    thr = np.minimum((cdf * 2 ** 32).astype(np.uint64), np.uint64(2 ** 32))
+    thr[-1] = np.uint64(2 ** 32)
+    u = uniform_labels(n, 1 << 31, seed).astype(np.uint64) << np.uint64(1)  # 32-bit uniform draw
+    return np.searchsorted(thr, u, side="right").astype(np.uint32)
+
+
+def random_walk_query(graph: "Graph", num_nodes: int, num_edges: int, seed: int = 1, max_tries: int = 1000) -> "Query":
+    """Query from a random walk in the data graph (SPEC random_walk_query S:63-71; PAPER P:220,
+    "uses random walks in the data graph to create a query graph of a specified size"): the
+    first num_nodes distinct vertices of a walk, the walk's edges kept first (connected), then
+    further edges of the induced subgraph in a seeded order until num_edges.  Labels are
+    inherited from the data graph (None if unlabeled).  Raises if no start succeeds."""
+    deg = np.diff(graph.offsets)
+    for t in range(max_tries):
+        start = int(draw(seed, 0x5257414c, t) % graph.num_nodes)
+        if deg[start] == 0:
+            continue
+        order, pos = [start], {start: 0}
+        edges = set()
+        cur = start
+        for step in range(64 * num_nodes):
+            if len(order) == num_nodes:
+                break
+            d = int(deg[cur])
+            if d == 0:
+                break
+            nxt = int(graph.cols[graph.offsets[cur] + draw(seed, 0x52574e58, t * 1_000_003 + step) % d])
+            if nxt not in pos:
+                pos[nxt] = len(order)
+                order.append(nxt)
+            a, b = pos[cur], pos[nxt]
+            if a != b:
+                edges.add((min(a, b), max(a, b)))
+            cur = nxt
+        if len(order) < num_nodes:
+            continue
+        # induced edges among the chosen vertices, in a seeded order
+        chosen = np.array(order, dtype=np.int64)
+        induced = []
+        for i, v in enumerate(order):
+            nb = graph.cols[graph.offsets[v]:graph.offsets[v + 1]]
+            for w in nb[np.isin(nb, chosen)]:
+                j = pos[int(w)]
+                if i < j:
+                    induced.append((i, j))
+        extra = [e for e in induced if e not in edges]
+        extra.sort(key=lambda e: draw(seed, 0x52574544, e[0] * 4096 + e[1]))
+        if len(edges) > num_edges or len(edges) + len(extra) < num_edges:
+            continue
+        edges = sorted(edges | set(extra[:num_edges - len(edges)]))
+        labels = None if graph.labels is None else [int(graph.labels[v]) for v in order]
+        return Query(num_nodes, edges, labels, f"rw{num_nodes}-{num_edges}-s{seed}")
+    raise RuntimeError("random walk did not reach the requested size; try another seed")
+
+
 def draw(seed: int, stream: int, idx: int) -> int:
     return int(_L().gen_draw(seed, stream, idx))
 

@@ -168,6 +168,26 @@ def test_ne_refinement_is_sound():
         G.free()
 
 
+def test_random_walk_queries_zipf_labels():
+    """Paper-shaped queries (random-walk queries on power-law labels):
+    GPU == oracle (count and rows) for 5..12-node queries; every query has >= 1 embedding
+    (the walk's own vertices)."""
+    g = gi.rmat(11, 16, seed=41).with_labels(gi.zipf_labels(2048, 20, 41))
+    G = load(g)
+    try:
+        for k, m in [(5, 6), (6, 8), (8, 12), (10, 16), (12, 22)]:
+            for s in range(3):
+                q = gi.random_walk_query(g, k, m, seed=97 * k + s)
+                cnt, ref = oracle.match(g, q)
+                assert cnt >= 1
+                c, rows, _ = run(G, q, "enumerate")
+                assert c == cnt, (q.name, c, cnt)
+                assert_rows_equal(rows, ref, q.name)
+                assert run(G, q, "count")[0] == cnt
+    finally:
+        G.free()
+
+
 def test_closed_forms_on_gpu():
     for n in (5, 8):
         G = load(gi.complete(n))

@@ -63,3 +63,37 @@ def test_grid_diagonal_counts(monkeypatch):
     cells = (W - 1) * (H - 1)
     assert abs(d2 / cells - 0.05) < 0.02 and abs(d1 / cells - 0.30) < 0.04
     assert g.num_edges == (W - 1) * H + W * (H - 1) + d1 + 2 * d2
+
+
+def test_zipf_labels_and_random_walk_queries(monkeypatch):
+    """SPEC assign_powerlaw_labels and random_walk_query."""
+    monkeypatch.setenv("GSM_CACHE_DIR", "off")
+    lab = gi.zipf_labels(200000, 20, seed=4)
+    assert lab.min() >= 0 and lab.max() <= 19
+    assert np.array_equal(lab, gi.zipf_labels(200000, 20, seed=4))
+    freq = np.bincount(lab, minlength=20) / len(lab)
+    h = sum(1.0 / (l + 1) for l in range(20))
+    for l in (0, 1, 4, 19):  # P(l) = (l+1)^-1 / H_20
+        assert abs(freq[l] - 1.0 / ((l + 1) * h)) < 0.01
+    assert np.all(gi.zipf_labels(1000, 1, 2) == 0)  # one label = unlabeled semantics (S:60)
+    g = gi.rmat(12, 16, seed=2).with_labels(gi.zipf_labels(4096, 20, 2))
+    for seed in range(5):
+        q = gi.random_walk_query(g, 12, 22, seed)
+        assert q.num_nodes == 12 and len(q.edges) == 22 and len(set(q.edges)) == 22
+        # connected
+        seen, stack = {0}, [0]
+        adj = {u: set() for u in range(12)}
+        for a, b in q.edges:
+            adj[a].add(b)
+            adj[b].add(a)
+        while stack:
+            for w in adj[stack.pop()]:
+                if w not in seen:
+                    seen.add(w)
+                    stack.append(w)
+        assert len(seen) == 12
+        assert q.labels is not None and len(q.labels) == 12
+        assert q.edges == gi.random_walk_query(g, 12, 22, seed).edges  # deterministic
+    # a triangle from K4 (SPEC S:69)
+    q3 = gi.random_walk_query(gi.complete(4), 3, 3, 1)
+    assert sorted(q3.edges) == [(0, 1), (0, 2), (1, 2)]

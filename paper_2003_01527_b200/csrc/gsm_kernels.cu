@@ -1072,27 +1072,7 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
             // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
             // enumerate the shorter side (measured: biasing towards B is slower)
-            if (nA >= 64 && nB >= 64 && a.rel > 0) {
-                // C: both sides long — sorted-list intersection: each lane takes a contiguous
-                // slice of RC after c and gallops forward through N(c) (O(nA + nB) total)
-                const int per = (int)((nA + 31) / 32);
-                const int x0 = j0 + lane * per, x1 = min(j1, x0 + per);
-                if (x0 < x1) {
-                    int64_t pos = lower_bound_cols(cols, s0, t0, (int64_t)(kb | rc[x0]));
-                    for (int j = x0; j < x1 && pos < t0; ++j) {
-                        const int32_t d = rc[j];
-                        ++items;
-                        pos = gallop(cols, pos, t0, kb | d, probes);
-                        if (pos >= t0 || cols[pos] != (kb | d)) continue;
-                        bool ok = true;
-                        if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
-                        for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
-                        for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
-                        for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
-                        cnt += ok;
-                    }
-                }
-            } else if (nB * 100 > (int64_t)a.bratio * nA) {
+            if (nB * 100 > (int64_t)a.bratio * nA) {
                 for (int j = j0 + lane; j < j1; j += 32) {
                     if (j == i) continue;
                     const int32_t d = rc[j];
@@ -1144,10 +1124,13 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
 // Big rows of the fused tail: one CTA per row, RC(r) (up to a.cap entries) built
 // block-wide in shared memory (order-preserving ballot compaction with a warp
 // scan per 256-candidate round), then the 8 warps split the c's of RC(r).
+constexpr int kTBThreads = 1024;  // 32 warps: the 160 KB RC buffer allows one CTA per SM
+constexpr int kTBWarps = kTBThreads / 32;
+
 template <typename MaskT>
-__global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan Lc, LevelPlan Ld) {
+__global__ void __launch_bounds__(kTBThreads) k_tail_block(TailArgs a, LevelPlan Lc, LevelPlan Ld) {
     extern __shared__ __align__(16) int32_t rcb[];
-    __shared__ int sWarpCnt[kWarps];
+    __shared__ int sWarpCnt[kTBWarps];
     __shared__ int sN;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -1172,7 +1155,7 @@ __global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan L
         __syncthreads();
         if (threadIdx.x == 0) sN = 0;
         __syncthreads();
-        for (int64_t base = 0; base < len; base += kThreads) {
+        for (int64_t base = 0; base < len; base += kTBThreads) {
             const int64_t i = base + threadIdx.x;
             bool ok = i < len;
             const int32_t v = ok ? (cols[beg + i] & idm) : 0;
@@ -1190,13 +1173,13 @@ __global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan L
             __syncthreads();
             if (threadIdx.x == 0) {
                 int tot = 0;
-                for (int w = 0; w < kWarps; ++w) tot += sWarpCnt[w];
+                for (int w = 0; w < kTBWarps; ++w) tot += sWarpCnt[w];
                 sN += tot;
             }
             __syncthreads();
         }
         const int n = sN;
-        for (int i = warp; i < n; i += kWarps) {
+        for (int i = warp; i < n; i += kTBWarps) {
             const int32_t c = rcb[i];
             bool okc = true;
             if (Lc.check_mask) okc = (cmask[c] >> Lc.qv) & 1u;
@@ -1221,27 +1204,7 @@ __global__ void __launch_bounds__(kThreads) k_tail_block(TailArgs a, LevelPlan L
             // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
             // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
             // enumerate the shorter side (measured: biasing towards B is slower)
-            if (nA >= 64 && nB >= 64 && a.rel > 0) {
-                // C: both sides long — sorted-list intersection: each lane takes a contiguous
-                // slice of RC after c and gallops forward through N(c) (O(nA + nB) total)
-                const int per = (int)((nA + 31) / 32);
-                const int x0 = j0 + lane * per, x1 = min(j1, x0 + per);
-                if (x0 < x1) {
-                    int64_t pos = lower_bound_cols(cols, s0, t0, (int64_t)(kb | rcb[x0]));
-                    for (int j = x0; j < x1 && pos < t0; ++j) {
-                        const int32_t d = rcb[j];
-                        ++items;
-                        pos = gallop(cols, pos, t0, kb | d, probes);
-                        if (pos >= t0 || cols[pos] != (kb | d)) continue;
-                        bool ok = true;
-                        if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
-                        for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
-                        for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
-                        for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
-                        cnt += ok;
-                    }
-                }
-            } else if (nB * 100 > (int64_t)a.bratio * nA) {
+            if (nB * 100 > (int64_t)a.bratio * nA) {
                 for (int j = j0 + lane; j < j1; j += 32) {
                     if (j == i) continue;
                     const int32_t d = rcb[j];
@@ -1296,9 +1259,9 @@ static void launch_tail_block_t(const TailArgs& a, const LevelPlan& Lc, const Le
     int dev = 0, sms = 148, per_sm = 1;
     GSM_CUDA(cudaGetDevice(&dev));
     GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_block<MaskT>, kThreads, smem));
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail_block<MaskT>, kTBThreads, smem));
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(a.R, (int64_t)sms * std::max(per_sm, 1)));
-    k_tail_block<MaskT><<<(unsigned)grid, kThreads, smem, s>>>(a, Lc, Ld);
+    k_tail_block<MaskT><<<(unsigned)grid, kTBThreads, smem, s>>>(a, Lc, Ld);
     GSM_LAUNCH("k_tail_block");
 }
 

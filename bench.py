@@ -41,6 +41,7 @@ def parse_args():
     p.add_argument("--e2e-steps", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
+    p.add_argument("--refine-rounds", type=int, default=0, help="NE filter rounds (Alg. 1 lines 7-8)")
     return p.parse_args()
 
 
@@ -218,8 +219,9 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
-def config_of(w, g):
+def config_of(w, g, refine_rounds=0):
     return {"workload": f"{w.name} (BASELINE configs[{w.config_index}]): {w.description}",
+            "refine_rounds": refine_rounds,
             "graph": {"name": g.name, "num_nodes": g.num_nodes, "directed_edges": g.nnz,
                       "csr_bytes": int(g.offsets.nbytes + g.cols.nbytes + (0 if g.labels is None else g.labels.nbytes))},
             "queries": [q.name for q in w.queries], "mode": "count, all embeddings (= |Aut(Q)| x orbit representatives)",
@@ -256,7 +258,8 @@ def run_ours(args, world, rank, local, dist):
         profs = []
         for q in w.queries:
             r = gsm.gsm_match(G_, q.num_nodes, q.edges, q.labels, mode=gsm.GSM_MODE_COUNT, flags=flags,
-                              shard_index=rank, num_shards=world, mem_budget_bytes=w.mem_budget_bytes, stream=sptr)
+                              shard_index=rank, num_shards=world, mem_budget_bytes=w.mem_budget_bytes, stream=sptr,
+                              refine_rounds=args.refine_rounds)
             tot_all += r.count
             tot_unique += r.count_unique
             launches += r.kernel_launches
@@ -367,7 +370,7 @@ def run_ours(args, world, rank, local, dist):
            **({"one_device_functional_check": True} if ONE_DEVICE else {}),
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-           "config": config_of(w, g),
+           "config": config_of(w, g, args.refine_rounds),
            "counts_per_step": {"all": c_all, "unique": c_uni},
            "unique_per_s": c_uni / (ms / 1000.0),
            "query_ms": ms, "per_query_rank0": per_query, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}

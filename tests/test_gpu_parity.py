@@ -172,7 +172,7 @@ def test_random_walk_queries_zipf_labels():
     """Paper-shaped queries (random-walk queries on power-law labels):
     GPU == oracle (count and rows) for 5..12-node queries; every query has >= 1 embedding
     (the walk's own vertices)."""
-    g = gi.rmat(11, 16, seed=41).with_labels(gi.zipf_labels(2048, 20, 41))
+    g = gi.rmat(9, 8, seed=41).with_labels(gi.zipf_labels(512, 20, 41))  # oracle < 2 s per query
     G = load(g)
     try:
         for k, m in [(5, 6), (6, 8), (8, 12), (10, 16), (12, 22)]:

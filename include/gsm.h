@@ -34,6 +34,10 @@
  * Threading: a gsm_graph is bound to one CUDA device and is not thread-safe;
  * use one handle per device per process.  gsm_match is synchronous with
  * respect to the host (it returns when its results are final).
+ *
+ * Memory: gsm_match keeps its grow-only device work buffers (frontier chunks,
+ * per-row plans, counters — at most mem_budget_bytes plus O(n)) inside the
+ * graph handle and reuses them on the next call; gsm_free releases them.
  */
 #ifndef GSM_H_
 #define GSM_H_

@@ -43,6 +43,12 @@ def raw_rows(rep):
     return header, units, rows
 
 
+def kname(raw):
+    """'void gsm::k_tail<unsigned char>(TailArgs, ...)' -> 'k_tail'"""
+    base = raw.split("(")[0].split("<")[0].strip()
+    return base.split()[-1].split("::")[-1]
+
+
 def to_float(x):
     try:
         return float(x.replace(",", ""))
@@ -53,10 +59,10 @@ def to_float(x):
 def full(rep, workload, alg=None):
     header, units, rows = raw_rows(rep)
     idx = {h: i for i, h in enumerate(header)}
-    kname = idx.get("Kernel Name")
+    kidx = idx.get("Kernel Name")
     per = defaultdict(list)
     for r in rows:
-        name = r[kname].split("(")[0].split("<")[0].strip()
+        name = kname(r[kidx])
         d = {}
         for m, key in METRICS.items():
             if m in idx:
@@ -99,7 +105,7 @@ def launches(csvpath, outmd):
     for r in rows:
         if len(r) < len(header) or r[idx["Metric Name"]] != "gpu__time_duration.sum":
             continue
-        name = r[idx["Kernel Name"]].split("(")[0].split("<")[0].strip()
+        name = kname(r[idx["Kernel Name"]])
         v = to_float(r[idx["Metric Value"]]) or 0.0
         unit = r[idx["Metric Unit"]]
         v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1e-3)
@@ -125,7 +131,7 @@ def metrics(csvpath, workload):
     for r in rows:
         if len(r) < len(header):
             continue
-        name = r[idx["Kernel Name"]].split("(")[0].split("<")[0].strip()
+        name = kname(r[idx["Kernel Name"]])
         m = r[idx["Metric Name"]]
         v = to_float(r[idx["Metric Value"]])
         u = r[idx["Metric Unit"]]

@@ -973,15 +973,15 @@ void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cuda
 // Rows whose pivot segment exceeds the per-warp buffer are handed back (overflow
 // list) to the generic BFS path.
 // ============================================================================
-// per-warp shared memory of k_tail: RC[cap]
-__host__ __device__ inline int tail_warp_ints(int cap) { return cap; }
+// per-warp shared memory of k_tail: RC[cap] + 64 x (int64 segment start, int32 length)
+__host__ __device__ inline int tail_warp_ints(int cap) { return ((cap + 1) & ~1) + 64 * 3; }
 
 template <typename MaskT>
 __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, LevelPlan Ld) {
     extern __shared__ __align__(16) int32_t tail_smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    int32_t* rc = tail_smem + wib * tail_warp_ints(a.cap);
+    int32_t* rc = tail_smem + wib * tail_warp_ints(a.cap);  // cap is even: the int64 part stays aligned
     const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
     const int32_t* __restrict__ cols = a.cols;
     const int W = Lc.width;
@@ -1020,6 +1020,19 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
         // ---- phase 2a: small RC with d ≻ c: the n(n-1)/2 pairs (c, d) = (RC[i], RC[j]), i < j,
         //      spread over the lanes (one independent search of d in N+(c) per lane)
         if (a.rel > 0 && !Lc.keyed && n <= 64) {
+            // per-c data once per row (not once per pair): N+(c) segment, or -1 if c fails
+            int64_t* cseg = reinterpret_cast<int64_t*>(rc + a.cap);
+            int32_t* clen = reinterpret_cast<int32_t*>(cseg + 64);
+            for (int i = lane; i < n; i += 32) {
+                const int32_t c = rc[i];
+                bool ok = true;
+                if (Lc.check_mask) ok = (cmask[c] >> Lc.qv) & 1u;
+                for (int q = 0; q < Lc.ninj && ok; ++q) ok = c != row[Lc.inj[q]];
+                const int64_t s0 = a.off[c] + a.up[c];
+                cseg[i] = s0;
+                clen[i] = ok ? (int32_t)(a.off[c + 1] - s0) : -1;
+            }
+            __syncwarp();
             const int np = n * (n - 1) / 2;
             for (int pidx = lane; pidx < np; pidx += 32) {
                 const float fn = 2.0f * n - 1.0f;
@@ -1028,19 +1041,16 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
                 while (i > 0 && i * (2 * n - i - 1) / 2 > pidx) --i;
                 while ((i + 1) * (2 * n - i - 2) / 2 <= pidx) ++i;
                 const int j = pidx - i * (2 * n - i - 1) / 2 + i + 1;
-                const int32_t c = rc[i], d = rc[j];
+                const int len = clen[i];
+                if (len <= 0) continue;
+                const int32_t d = rc[j];
                 ++items;
                 bool ok = true;
-                if (Lc.check_mask) ok = (cmask[c] >> Lc.qv) & 1u;
-                for (int q = 0; q < Lc.ninj && ok; ++q) ok = c != row[Lc.inj[q]];
-                if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
                 for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
                 for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
                 for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
-                if (ok) {
-                    const int64_t s0 = a.off[c] + a.up[c], t0 = a.off[c + 1];
-                    ok = in_sorted(cols + s0, (int)(t0 - s0), d, probes);
-                }
+                if (ok) ok = in_sorted(cols + cseg[i], len, d, probes);
                 cnt += ok;
             }
             __syncwarp();
@@ -1289,9 +1299,9 @@ int tail_bratio() {  // phase-2 strategy, in percent: stream N(c) (B) when |N(c)
 int tail_cap() {  // per-warp candidate buffer; GSM_TAIL_CAP (tests force the overflow path with it)
     const char* v = getenv("GSM_TAIL_CAP");
     int cap = (v && *v) ? atoi(v) : 1024;
-    if (cap < 32) cap = 32;
+    if (cap < 64) cap = 64;
     if (cap > 6144) cap = 6144;
-    return cap;
+    return cap & ~1;  // even: keeps the per-warp int64 area aligned
 }
 
 template <typename MaskT>

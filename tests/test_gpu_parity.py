@@ -117,15 +117,15 @@ def test_labeled_named_queries():
         G.free()
 
 
-@pytest.mark.parametrize("tail", ["0", "1", "cap32", "cap32block256"])
+@pytest.mark.parametrize("tail", ["0", "1", "cap64", "cap64block256"])
 def test_fused_tail_matches_generic_path(tail, monkeypatch):
     """The fused last-two-positions kernel (COUNT mode, clique-like tails) against the
     oracle, with the fusion disabled, enabled, and enabled with a tiny per-warp buffer
     (forcing the overflow hand-back to the generic path)."""
     monkeypatch.setenv("GSM_FUSED_TAIL", "0" if tail == "0" else "1")
-    if tail.startswith("cap32"):
-        monkeypatch.setenv("GSM_TAIL_CAP", "32")
-    if tail == "cap32block256":
+    if tail.startswith("cap64"):
+        monkeypatch.setenv("GSM_TAIL_CAP", "64")
+    if tail == "cap64block256":
         monkeypatch.setenv("GSM_TAIL_BLOCK_CAP", "256")
     g = gi.rmat(10, 16, seed=12).with_labels(gi.uniform_labels(1024, 2, 12))
     G = load(g)

@@ -96,8 +96,16 @@ class ClockSampler:
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        if not sm:  # timed region shorter than one 200 ms sample: one query right after it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=30)
+                parts = [x.strip() for x in out.stdout.strip().split(",")]
+                reasons = sorted(nm for nm, v in zip(names, parts[3:7]) if v.lower().startswith("active"))
+                return {"sm_mhz": float(parts[0]), "sm_max_mhz": float(parts[1]), "reasons": reasons,
+                        "samples": 0, "note": "timed region < 200 ms; sampled once right after it"}
+            except Exception:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
                 "samples": len(sm)}
 
@@ -264,6 +272,8 @@ def run_ours(args, world, rank, local, dist):
             tot_unique += r.count_unique
             launches += r.kernel_launches
             profs.append(r.prof)
+            if G_ is not G:
+                continue  # e2e steps (fresh graph each step) do not overwrite the resident-graph stats
             per_query[q.name] = {"count": r.count, "unique": r.count_unique, "automorphisms": r.automorphisms,
                                  "order": r.order, "candidates": r.candidates, "level_work": r.level_work,
                                  "level_rows": r.level_rows, "chunks": r.num_chunks,

@@ -989,9 +989,20 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
     const int32_t kb = Lc.key_base, idm = Lc.idmask;
     unsigned long long cnt = 0, items = 0, probes_u = 0;
     unsigned probes = 0;
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = gw; r < a.R; r += nw) {
+    // dynamic row scheduling: row costs vary by orders of magnitude (|RC|^2), so warps
+    // grab chunks of rows from a global counter instead of a static stride
+    constexpr int64_t kChunk = 8;
+    int64_t cbase = 0, cend = 0;
+    for (;;) {
+        if (cbase >= cend) {
+            unsigned long long b = 0;
+            if (lane == 0) b = atomicAdd(a.next, (unsigned long long)kChunk);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if ((int64_t)b >= a.R) break;
+            cbase = (int64_t)b;
+            cend = min(cbase + kChunk, a.R);
+        }
+        const int64_t r = cbase++;
         const int64_t len = a.rlen[r];
         if (len == 0) continue;
         if (len > a.cap) {
@@ -1151,7 +1162,13 @@ __global__ void __launch_bounds__(kTBThreads) k_tail_block(TailArgs a, LevelPlan
     const int32_t kb = Lc.key_base, idm = Lc.idmask;
     unsigned long long cnt = 0, items = 0;
     unsigned probes = 0;
-    for (int64_t ri = blockIdx.x; ri < a.R; ri += gridDim.x) {
+    __shared__ unsigned long long sNext;
+    for (;;) {  // dynamic: one row at a time from a global counter (rows sorted largest first)
+        __syncthreads();
+        if (threadIdx.x == 0) sNext = atomicAdd(a.next, 1ull);
+        __syncthreads();
+        const int64_t ri = (int64_t)sNext;
+        if (ri >= a.R) break;
         const int64_t r = a.rows_idx ? a.rows_idx[ri] : ri;
         const int64_t len = a.rlen[r];
         if (len == 0) continue;  // block-uniform
@@ -1289,6 +1306,28 @@ int tail_block_cap() {  // per-CTA buffer for big rows (GSM_TAIL_BLOCK_CAP)
     if (cap < 256) cap = 256;
     if (cap > 48 * 1024) cap = 48 * 1024;
     return cap;
+}
+
+__global__ void k_gather_len(const int64_t* __restrict__ rlen, const int64_t* __restrict__ idx, int64_t n,
+                             int64_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = rlen[idx[i]];
+}
+
+void sort_rows_by_len_desc(const int64_t* rlen, int64_t* idx, int64_t n, cudaStream_t s) {
+    if (n <= 1) return;
+    DevBuf<int64_t> k_in, k_out, v_out;
+    k_in.ensure(n, s);
+    k_out.ensure(n, s);
+    v_out.ensure(n, s);
+    k_gather_len<<<grid_for(n), kThreads, 0, s>>>(rlen, idx, n, k_in.p);
+    GSM_LAUNCH("k_gather_len");
+    size_t tb = 0;
+    GSM_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, k_in.p, k_out.p, idx, v_out.p, n, 0, 40, s));
+    DevBuf<uint8_t> tmp;
+    tmp.ensure(tb, s);
+    GSM_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, k_in.p, k_out.p, idx, v_out.p, n, 0, 40, s));
+    GSM_CUDA(cudaMemcpyAsync(idx, v_out.p, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, s));
 }
 
 int tail_bratio() {  // phase-2 strategy, in percent: stream N(c) (B) when |N(c)| <= pct/100 x |RC part|

@@ -101,8 +101,11 @@ struct TailArgs {
     const int64_t* rows_idx;  // k_tail_block: indices of the rows to process (NULL = 0..R-1)
     int64_t* overflow;      // rows left to the next stage
     unsigned long long* noverflow;
+    unsigned long long* next;  // dynamic row scheduler (zeroed before each launch)
     unsigned long long* stats;
 };
+// Reorders row indices by descending pivot length (largest rows first: better makespan).
+void sort_rows_by_len_desc(const int64_t* rlen, int64_t* idx, int64_t n, cudaStream_t s);
 int tail_cap();
 int tail_bratio();
 int tail_block_cap();

@@ -383,6 +383,9 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
     a.count = final_count_.p;
     a.overflow = ovf_idx_.p;
     a.noverflow = ovf_n_.p;
+    ws_.sched.ensure(1, s_);
+    GSM_CUDA(cudaMemsetAsync(ws_.sched.p, 0, sizeof(unsigned long long), s_));
+    a.next = ws_.sched.p;
     a.stats = stats_.p + 5 * (kMaxK + 0);  // tail counters: slot kMaxK
     rec_.run(GSM_K_TAIL, 1, [&] { launch_tail(a, L, lplan_[w + 1], mask_bytes_, s_); });
     res_->num_chunks++;
@@ -393,6 +396,9 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
         idx.ensure(nov, s_);
         GSM_CUDA(cudaMemcpyAsync(idx.p, ovf_idx_.p, sizeof(int64_t) * nov, cudaMemcpyDeviceToDevice, s_));
         GSM_CUDA(cudaMemsetAsync(ovf_n_.p, 0, sizeof(unsigned long long), s_));
+        sort_rows_by_len_desc(B.rlen.p, idx.p, nov, s_);  // largest rows first
+        res_->kernel_launches += 5;
+        GSM_CUDA(cudaMemsetAsync(ws_.sched.p, 0, sizeof(unsigned long long), s_));
         TailArgs b = a;
         b.R = nov;
         b.rows_idx = idx.p;

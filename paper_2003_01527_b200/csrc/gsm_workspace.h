@@ -24,7 +24,7 @@ struct LevelBufs {
 struct Workspace {
     std::vector<std::unique_ptr<LevelBufs>> lv;  // index = frontier width 1..k
     DevBuf<uint8_t> cmask;
-    DevBuf<unsigned long long> counts, final_count, stats, ovf_n;
+    DevBuf<unsigned long long> counts, final_count, stats, ovf_n, sched;
     DevBuf<int64_t> ovf_idx;
     DevBuf<int32_t> ovf_rows;
     Workspace() : lv(kMaxK + 1) {

@@ -993,6 +993,8 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
     // grab chunks of rows from a global counter instead of a static stride
     constexpr int64_t kChunk = 8;
     int64_t cbase = 0, cend = 0;
+    unsigned long long cyc_p1 = 0, cyc_small = 0, cyc_big = 0, rows_small = 0, rows_big = 0;
+    long long t_row = 0, t_p1 = 0;
     for (;;) {
         if (cbase >= cend) {
             unsigned long long b = 0;
@@ -1012,6 +1014,7 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
         const int32_t* row = a.F + r * W;
         const int piv = a.rpiv[r];
         const int64_t beg = a.rbeg[r];
+        if (a.cyc) t_row = clock64();
         // ---- phase 1: RC(r) = pivot entries present in every other backward list (order kept)
         int n = 0;
         for (int64_t base = 0; base < len; base += 32) {
@@ -1028,6 +1031,10 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             n += __popc(ball);
         }
         __syncwarp();
+        if (a.cyc) {
+            t_p1 = clock64();
+            cyc_p1 += (unsigned long long)(t_p1 - t_row);
+        }
         // ---- phase 2a: small RC with d ≻ c: the n(n-1)/2 pairs (c, d) = (RC[i], RC[j]), i < j,
         //      spread over the lanes (one independent search of d in N+(c) per lane)
         if (a.rel > 0 && !Lc.keyed && n <= 64) {
@@ -1065,6 +1072,10 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
                 cnt += ok;
             }
             __syncwarp();
+            if (a.cyc) {
+                cyc_small += (unsigned long long)(clock64() - t_p1);
+                ++rows_small;
+            }
             continue;
         }
         // ---- phase 2b: pairs (c, d) inside RC(r), one c at a time across the warp
@@ -1125,6 +1136,17 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             }
         }
         __syncwarp();
+        if (a.cyc) {
+            cyc_big += (unsigned long long)(clock64() - t_p1);
+            ++rows_big;
+        }
+    }
+    if (a.cyc && lane == 0) {
+        atomicAdd(&a.cyc[0], cyc_p1);
+        atomicAdd(&a.cyc[1], cyc_small);
+        atomicAdd(&a.cyc[2], cyc_big);
+        atomicAdd(&a.cyc[3], rows_small);
+        atomicAdd(&a.cyc[4], rows_big);
     }
     probes_u = probes;
     for (int o = 16; o; o >>= 1) {

@@ -102,6 +102,7 @@ struct TailArgs {
     int64_t* overflow;      // rows left to the next stage
     unsigned long long* noverflow;
     unsigned long long* next;  // dynamic row scheduler (zeroed before each launch)
+    unsigned long long* cyc;   // optional (GSM_TRACE=2): warp cycles [phase1, small-RC pairs, big-RC c loop, #small, #big]
     unsigned long long* stats;
 };
 // Reorders row indices by descending pivot length (largest rows first: better makespan).

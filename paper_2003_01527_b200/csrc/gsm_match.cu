@@ -386,11 +386,26 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
     ws_.sched.ensure(1, s_);
     GSM_CUDA(cudaMemsetAsync(ws_.sched.p, 0, sizeof(unsigned long long), s_));
     a.next = ws_.sched.p;
+    const char* trace = getenv("GSM_TRACE");
+    DevBuf<unsigned long long> cyc;
+    if (trace && trace[0] == '2') {
+        cyc.ensure(8, s_);
+        GSM_CUDA(cudaMemsetAsync(cyc.p, 0, sizeof(unsigned long long) * 8, s_));
+        a.cyc = cyc.p;
+    }
     a.stats = stats_.p + 5 * (kMaxK + 0);  // tail counters: slot kMaxK
     rec_.run(GSM_K_TAIL, 1, [&] { launch_tail(a, L, lplan_[w + 1], mask_bytes_, s_); });
     res_->num_chunks++;
     tail_rows_ += (double)R;
     int64_t nov = (int64_t)read_scalar(ovf_n_.p, s_);
+    if (a.cyc) {
+        unsigned long long hc[8];
+        GSM_CUDA(cudaMemcpyAsync(hc, cyc.p, sizeof(hc), cudaMemcpyDeviceToHost, s_));
+        GSM_CUDA(cudaStreamSynchronize(s_));
+        std::fprintf(stderr, "[gsm tail] rows %lld: warp-cycles phase1 %.3g, small-RC pairs %.3g (%llu rows), "
+                     "big-RC %.3g (%llu rows), overflow rows %lld\n", (long long)R, (double)hc[0], (double)hc[1],
+                     hc[3], (double)hc[2], hc[4], (long long)nov);
+    }
     if (nov > 0) {  // rows whose list did not fit a warp's buffer: one CTA per row
         DevBuf<int64_t> idx;
         idx.ensure(nov, s_);

@@ -1078,60 +1078,79 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             }
             continue;
         }
-        // ---- phase 2b: pairs (c, d) inside RC(r), one c at a time across the warp
-        for (int i = 0; i < n; ++i) {
-            const int32_t c = rc[i];
-            bool okc = true;
-            if (Lc.check_mask) okc = (cmask[c] >> Lc.qv) & 1u;
-            for (int q = 0; q < Lc.ninj && okc; ++q) okc = c != row[Lc.inj[q]];
-            if (!okc) continue;  // warp-uniform
-            int j0 = 0, j1 = n;
-            if (a.rel > 0) j0 = i + 1;
-            else if (a.rel < 0) j1 = i;
-            if (j1 <= j0) continue;
-            const int64_t cs = a.off[c], ce = a.off[c + 1];
-            int64_t s0, t0;
-            if (!Lc.keyed && a.rel != 0) {  // d ≻ c (or ≺ c): exactly N+(c) (or N-(c)) via up[c], no search
-                const int64_t split = cs + a.up[c];
-                s0 = a.rel > 0 ? split : cs;
-                t0 = a.rel > 0 ? ce : split;
-            } else {
-                s0 = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rc[j0]));
-                t0 = lower_bound_cols(cols, s0, ce, (int64_t)(kb | rc[j1 - 1]) + 1);
-            }
-            const int64_t nA = j1 - j0, nB = t0 - s0;
-            if (nB <= 0) continue;
-            // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
-            // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
-            // enumerate the shorter side (measured: biasing towards B is slower)
-            if (nB * 100 > (int64_t)a.bratio * nA) {
-                for (int j = j0 + lane; j < j1; j += 32) {
-                    if (j == i) continue;
-                    const int32_t d = rc[j];
-                    ++items;
-                    bool ok = true;
-                    if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
-                    for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
-                    for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
-                    for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
-                    if (ok) ok = in_sorted(cols + s0, (int)nB, kb | d, probes);
-                    cnt += ok;
+        // ---- phase 2b: pairs (c, d) inside RC(r), one c at a time across the warp.  The per-c
+        //      data (filters, admissible part of N(c)) is fetched 32 c's at a time — lane l for
+        //      c = RC[g + l] — and broadcast by shuffles, so the warp never waits on a
+        //      serialized chain of per-c global loads.
+        for (int g0 = 0; g0 < n; g0 += 32) {
+            const int il = g0 + lane;
+            bool okl = false;
+            int64_t sl = 0, tl = 0;
+            if (il < n) {
+                const int32_t cl = rc[il];
+                okl = true;
+                if (Lc.check_mask) okl = (cmask[cl] >> Lc.qv) & 1u;
+                for (int q = 0; q < Lc.ninj && okl; ++q) okl = cl != row[Lc.inj[q]];
+                int j0 = 0, j1 = n;
+                if (a.rel > 0) j0 = il + 1;
+                else if (a.rel < 0) j1 = il;
+                if (j1 <= j0) okl = false;
+                if (okl) {
+                    const int64_t cs = a.off[cl], ce = a.off[cl + 1];
+                    if (!Lc.keyed && a.rel != 0) {  // d ≻ c (or ≺ c): exactly N+(c) (or N-(c)) via up[c]
+                        const int64_t split = cs + a.up[cl];
+                        sl = a.rel > 0 ? split : cs;
+                        tl = a.rel > 0 ? ce : split;
+                    } else {
+                        sl = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rc[j0]));
+                        tl = lower_bound_cols(cols, sl, ce, (int64_t)(kb | rc[j1 - 1]) + 1);
+                    }
+                    if (tl <= sl) okl = false;
                 }
-            } else {
-                const int32_t dmax = rc[j1 - 1];
-                for (int64_t x0 = s0; x0 < t0; x0 += 32) {
-                    const int64_t x = x0 + lane;
-                    const int32_t d = x < t0 ? (cols[x] & idm) : INT32_MAX;
-                    if (!__any_sync(0xffffffffu, d <= dmax)) break;  // N(c) is sorted: past max RC
-                    if (d > dmax) continue;
-                    ++items;
-                    unsigned dummy = 0;
-                    bool ok = d != c && in_sorted(rc + j0, j1 - j0, d, dummy);
-                    if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
-                    for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
-                    for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
-                    for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
-                    cnt += ok;
+            }
+            const unsigned live = __ballot_sync(0xffffffffu, okl);
+            for (int ii = 0; ii < 32; ++ii) {
+                if (!((live >> ii) & 1u)) continue;  // warp-uniform
+                const int i = g0 + ii;
+                const int32_t c = rc[i];
+                const int64_t s0 = __shfl_sync(0xffffffffu, sl, ii);
+                const int64_t t0 = __shfl_sync(0xffffffffu, tl, ii);
+                int j0 = 0, j1 = n;
+                if (a.rel > 0) j0 = i + 1;
+                else if (a.rel < 0) j1 = i;
+                const int64_t nA = j1 - j0, nB = t0 - s0;
+                // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
+                // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
+                // enumerate the shorter side (measured: biasing towards B is slower)
+                if (nB * 100 > (int64_t)a.bratio * nA) {
+                    for (int j = j0 + lane; j < j1; j += 32) {
+                        if (j == i) continue;
+                        const int32_t d = rc[j];
+                        ++items;
+                        bool ok = true;
+                        if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                        for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                        for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                        for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                        if (ok) ok = in_sorted(cols + s0, (int)nB, kb | d, probes);
+                        cnt += ok;
+                    }
+                } else {
+                    const int32_t dmax = rc[j1 - 1];
+                    for (int64_t x0 = s0; x0 < t0; x0 += 32) {
+                        const int64_t x = x0 + lane;
+                        const int32_t d = x < t0 ? (cols[x] & idm) : INT32_MAX;
+                        if (!__any_sync(0xffffffffu, d <= dmax)) break;  // N(c) is sorted: past max RC
+                        if (d > dmax) continue;
+                        ++items;
+                        unsigned dummy = 0;
+                        bool ok = d != c && in_sorted(rc + j0, j1 - j0, d, dummy);
+                        if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                        for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                        for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                        for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                        cnt += ok;
+                    }
                 }
             }
         }
@@ -1228,59 +1247,77 @@ __global__ void __launch_bounds__(kTBThreads) k_tail_block(TailArgs a, LevelPlan
             __syncthreads();
         }
         const int n = sN;
-        for (int i = warp; i < n; i += kTBWarps) {
-            const int32_t c = rcb[i];
-            bool okc = true;
-            if (Lc.check_mask) okc = (cmask[c] >> Lc.qv) & 1u;
-            for (int q = 0; q < Lc.ninj && okc; ++q) okc = c != row[Lc.inj[q]];
-            if (!okc) continue;
-            int j0 = 0, j1 = n;
-            if (a.rel > 0) j0 = i + 1;
-            else if (a.rel < 0) j1 = i;
-            if (j1 <= j0) continue;
-            const int64_t cs = a.off[c], ce = a.off[c + 1];
-            int64_t s0, t0;
-            if (!Lc.keyed && a.rel != 0) {
-                const int64_t split = cs + a.up[c];
-                s0 = a.rel > 0 ? split : cs;
-                t0 = a.rel > 0 ? ce : split;
-            } else {
-                s0 = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rcb[j0]));
-                t0 = lower_bound_cols(cols, s0, ce, (int64_t)(kb | rcb[j1 - 1]) + 1);
-            }
-            const int64_t nA = j1 - j0, nB = t0 - s0;
-            if (nB <= 0) continue;
-            // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
-            // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
-            // enumerate the shorter side (measured: biasing towards B is slower)
-            if (nB * 100 > (int64_t)a.bratio * nA) {
-                for (int j = j0 + lane; j < j1; j += 32) {
-                    if (j == i) continue;
-                    const int32_t d = rcb[j];
-                    ++items;
-                    bool ok = true;
-                    if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
-                    for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
-                    for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
-                    for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
-                    if (ok) ok = in_sorted(cols + s0, (int)nB, kb | d, probes);
-                    cnt += ok;
+        // this warp's c's: i = warp, warp + 32, ...; per-c data fetched 32 c's at a time (lane l
+        // for the warp's (g + l)-th c) and broadcast by shuffles
+        for (int g0 = 0; warp + kTBWarps * g0 < n; g0 += 32) {
+            const int il = warp + kTBWarps * (g0 + lane);
+            bool okl = false;
+            int64_t sl = 0, tl = 0;
+            if (il < n) {
+                const int32_t cl = rcb[il];
+                okl = true;
+                if (Lc.check_mask) okl = (cmask[cl] >> Lc.qv) & 1u;
+                for (int q = 0; q < Lc.ninj && okl; ++q) okl = cl != row[Lc.inj[q]];
+                int j0 = 0, j1 = n;
+                if (a.rel > 0) j0 = il + 1;
+                else if (a.rel < 0) j1 = il;
+                if (j1 <= j0) okl = false;
+                if (okl) {
+                    const int64_t cs = a.off[cl], ce = a.off[cl + 1];
+                    if (!Lc.keyed && a.rel != 0) {
+                        const int64_t split = cs + a.up[cl];
+                        sl = a.rel > 0 ? split : cs;
+                        tl = a.rel > 0 ? ce : split;
+                    } else {
+                        sl = lower_bound_cols(cols, cs, ce, (int64_t)(kb | rcb[j0]));
+                        tl = lower_bound_cols(cols, sl, ce, (int64_t)(kb | rcb[j1 - 1]) + 1);
+                    }
+                    if (tl <= sl) okl = false;
                 }
-            } else {
-                const int32_t dmax = rcb[j1 - 1];
-                for (int64_t x0 = s0; x0 < t0; x0 += 32) {
-                    const int64_t x = x0 + lane;
-                    const int32_t d = x < t0 ? (cols[x] & idm) : INT32_MAX;
-                    if (!__any_sync(0xffffffffu, d <= dmax)) break;  // N(c) is sorted: past max RC
-                    if (d > dmax) continue;
-                    ++items;
-                    unsigned dummy = 0;
-                    bool ok = d != c && in_sorted(rcb + j0, j1 - j0, d, dummy);
-                    if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
-                    for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
-                    for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
-                    for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
-                    cnt += ok;
+            }
+            const unsigned live = __ballot_sync(0xffffffffu, okl);
+            for (int ii = 0; ii < 32; ++ii) {
+                if (!((live >> ii) & 1u)) continue;  // warp-uniform
+                const int i = warp + kTBWarps * (g0 + ii);
+                const int32_t c = rcb[i];
+                const int64_t s0 = __shfl_sync(0xffffffffu, sl, ii);
+                const int64_t t0 = __shfl_sync(0xffffffffu, tl, ii);
+                int j0 = 0, j1 = n;
+                if (a.rel > 0) j0 = i + 1;
+                else if (a.rel < 0) j1 = i;
+                const int64_t nA = j1 - j0, nB = t0 - s0;
+                // A (search RC's entries in N(c): global binary searches, mostly L1/L2 hits) vs
+                // B (stream N(c), search each entry in RC in shared memory, stop past max RC):
+                // enumerate the shorter side (measured: biasing towards B is slower)
+                if (nB * 100 > (int64_t)a.bratio * nA) {
+                    for (int j = j0 + lane; j < j1; j += 32) {
+                        if (j == i) continue;
+                        const int32_t d = rcb[j];
+                        ++items;
+                        bool ok = true;
+                        if (Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                        for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                        for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                        for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                        if (ok) ok = in_sorted(cols + s0, (int)nB, kb | d, probes);
+                        cnt += ok;
+                    }
+                } else {
+                    const int32_t dmax = rcb[j1 - 1];
+                    for (int64_t x0 = s0; x0 < t0; x0 += 32) {
+                        const int64_t x = x0 + lane;
+                        const int32_t d = x < t0 ? (cols[x] & idm) : INT32_MAX;
+                        if (!__any_sync(0xffffffffu, d <= dmax)) break;  // N(c) is sorted: past max RC
+                        if (d > dmax) continue;
+                        ++items;
+                        unsigned dummy = 0;
+                        bool ok = d != c && in_sorted(rcb + j0, j1 - j0, d, dummy);
+                        if (ok && Ld.check_mask) ok = (cmask[d] >> Ld.qv) & 1u;
+                        for (int q = 0; q < a.nxlo && ok; ++q) ok = d > row[a.xlo[q]];
+                        for (int q = 0; q < a.nxhi && ok; ++q) ok = d < row[a.xhi[q]];
+                        for (int q = 0; q < Ld.ninj && ok; ++q) ok = d != row[Ld.inj[q]];
+                        cnt += ok;
+                    }
                 }
             }
         }

@@ -249,7 +249,14 @@ def run_ours(args, world, rank, local, dist):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = workloads.get(args.workload)
-    g = w.graph()
+    if dist is not None:  # rank 0 generates (all host cores) and fills the on-disk cache; the others load it
+        if rank == 0:
+            g = w.graph()
+        dist.barrier()
+        if rank != 0:
+            g = w.graph()
+    else:
+        g = w.graph()
     G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=local)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream

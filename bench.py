@@ -140,7 +140,8 @@ def load_peaks():
         return {}
 
 
-KERNELS_OF = {"expand": ["k_expand", "k_count_walk"], "tail": ["k_tail", "k_tail_block"], "filter": ["k_filter"],
+KERNELS_OF = {"expand": ["k_expand", "k_count_walk"], "tail": ["k_tail", "k_tail_block"],
+              "clique": ["k_clique_cta", "k_clique_warp"], "filter": ["k_filter"],
               "plan": ["k_plan_rows"], "roots": ["k_root_count", "k_root_write"]}
 
 

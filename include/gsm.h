@@ -173,7 +173,8 @@ enum {
     GSM_K_EXPAND = 4,   /* K2/K3/K4 expand + verify + compact            */
     GSM_K_FINALIZE = 5, /* id map, Aut expansion, radix sort             */
     GSM_K_TAIL = 6,     /* fused last two positions (COUNT mode, clique-like tails) */
-    GSM_K_COUNT_ = 7
+    GSM_K_CLIQUE = 7,   /* clique queries K3/K4 (COUNT mode): per-root local bitmaps */
+    GSM_K_COUNT_ = 8
 };
 
 typedef struct {

@@ -1,0 +1,463 @@
+// gsm_clique.cu — COUNT mode for clique queries K_k (k = 3, 4): the verify step
+// on per-root local bitmaps.
+//
+// Which query: every position i >= 1 is adjacent to all earlier positions
+// (B(i) = {0..i-1}) and the symmetry conditions (Grochow-Kellis, DESIGN R9)
+// chain f(π[0]) ≺ f(π[1]) ≺ ... ≺ f(π[k-1]); unlabeled.  Then every partial
+// result (u = f(π[0]), f(π[1]), ...) lives inside S(u) = N+(u) = {w ∈ N(u): w ≻ u}
+// (≺ = relabelled-id order, so N+(u) is the suffix of u's sorted list at up[u]).
+//
+// Same search tree as Alg. 1: level 1 extends root u by a ∈ S(u);
+// level i extends (u, a1, .., a_{i-1}) by the candidates of the pivot list that
+// are connected to every earlier position ("connections with existing nodes
+// in partial results").  What changes is the representation of the candidate
+// sets: per root, the connection test "w ∈ N(S[i])" for w ∈ S(u) is evaluated
+// ONCE into a bit row A[i] (bit j set iff S[j] ∈ N+(S[i]), j > i), and the
+// candidate set of a partial result is the AND of the rows of its members.
+// For K4 the last level counts popc(A[i] & A[j]) over the level-2 partial results
+// (u, S[i], S[j]) — the width-3 frontier is never materialised, and each
+// verification of two backward edges of 32 candidates is one AND + POPC.
+//
+// Work split (roots sorted by |S(u)| descending, dynamic scheduling):
+//   d <= 32     k_clique_warp: one warp per root, lane i holds row A[i] (1 word)
+//   d <= dsmem  k_clique_cta : one CTA per root, S and A in shared memory
+//   larger      k_clique_cta<kGlobal>: S and A in a per-CTA global slab (L2)
+// Row construction per i picks the cheaper of (a) the lanes binary-searching
+// their S[j] in N+(S[i]) (global, mostly L1/L2 hits) and (b) streaming N+(S[i])
+// (coalesced) and binary-searching each entry in S (shared memory).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "gsm_kernels.h"
+
+namespace gsm {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// key ∈ cols[lo, hi) (sorted), by binary search
+__device__ __forceinline__ bool search_list(const int32_t* __restrict__ cols, int64_t lo, int64_t hi, int32_t key,
+                                            unsigned& probes) {
+    int64_t l = lo, h = hi;
+    while (l < h) {
+        const int64_t mid = (l + h) >> 1;
+        ++probes;
+        if (__ldg(cols + mid) < key) l = mid + 1; else h = mid;
+    }
+    return l < hi && __ldg(cols + l) == key;
+}
+
+// index of key in S[lo, hi) or -1
+__device__ __forceinline__ int search_local(const int32_t* S, int lo, int hi, int32_t key) {
+    int l = lo, h = hi;
+    while (l < h) {
+        const int mid = (l + h) >> 1;
+        if (S[mid] < key) l = mid + 1; else h = mid;
+    }
+    return (l < hi && S[l] == key) ? l : -1;
+}
+
+__device__ __forceinline__ int slab_ints(int dmax) {
+    const int W = (dmax + 31) >> 5;
+    return dmax + dmax * (W | 1);
+}
+
+}  // namespace
+
+// keys[r] = |N+(roots[r])| (0 if below k-1: no clique through it), vals[r] = r;
+// bucket counts (d <= wmax: warp; d > dsmem: global slab; else d <= 128, <= 512, <= dsmem)
+// and the max.  Descending keys keep every bucket contiguous in the sorted order.
+__global__ void k_clique_keys(const int32_t* __restrict__ roots, int64_t R, const int64_t* __restrict__ off,
+                              const int32_t* __restrict__ up, int kmin, int wmax, int dsmem,
+                              int32_t* __restrict__ keys,
+                              int32_t* __restrict__ vals, unsigned long long* __restrict__ bucket, int* dmax) {
+    __shared__ unsigned long long sb[5];
+    __shared__ int sm;
+    if (threadIdx.x < 5) sb[threadIdx.x] = 0;
+    if (threadIdx.x == 0) sm = 0;
+    __syncthreads();
+    int lm = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t u = roots[r];
+        int d = (int)(off[u + 1] - off[u] - up[u]);
+        if (d < kmin) d = 0;
+        keys[r] = d;
+        vals[r] = (int32_t)r;
+        if (d > 0) {
+            const int b = d <= wmax ? 0 : d > dsmem ? 4 : d <= 128 ? 1 : d <= 512 ? 2 : 3;
+            atomicAdd(&sb[b], 1ull);
+            lm = max(lm, d);
+        }
+    }
+    atomicMax(&sm, lm);
+    __syncthreads();
+    if (threadIdx.x < 5 && sb[threadIdx.x]) atomicAdd(&bucket[threadIdx.x], sb[threadIdx.x]);
+    if (threadIdx.x == 0 && sm) atomicMax(dmax, sm);
+}
+
+struct CliqueArgs {
+    const int32_t* roots;   // level-0 frontier (new ids)
+    const int32_t* idx;     // roots of this launch: roots[idx[t]], t < n
+    int64_t n;
+    const int64_t* off;
+    const int32_t* cols;
+    const int32_t* up;
+    int32_t dmax;           // max |N+(u)| of this launch (sizes shared memory / the slab)
+    int32_t stream_max;     // row construction streams N+(S[i]) when its length <= stream_max * (#j)/32
+    int32_t* slab;          // kGlobal: per-CTA scratch of slab_ints(dmax) ints
+    unsigned long long* next;   // dynamic root scheduler
+    unsigned long long* count;  // unique cliques (atomic)
+    unsigned long long* stats;  // [list entries read, global probes, bitmap words, cliques, sum |S(u)|]
+};
+
+// ---------------------------------------------------------------------------- d <= 32
+template <int K>
+__global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
+    __shared__ int32_t sS[8][32];
+    __shared__ unsigned sA[8][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int32_t* __restrict__ cols = a.cols;
+    unsigned long long cnt = 0, items = 0, sent = 0;
+    unsigned probes = 0;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t t = (int64_t)blockIdx.x * 8 + wib; t < a.n; t += nw) {
+        const int32_t u = a.roots[a.idx[t]];
+        const int64_t s0 = a.off[u] + a.up[u];
+        const int d = (int)(a.off[u + 1] - s0);
+        const int32_t sv = lane < d ? cols[s0 + lane] : INT32_MAX;
+        sS[wib][lane] = sv;
+        if (lane == 0) sent += d;
+        __syncwarp();
+        const int32_t smax = sS[wib][d - 1];
+        unsigned myrow = 0;
+        for (int i = 0; i < d - 1; ++i) {
+            const int32_t ai = sS[wib][i];
+            const int64_t ls = a.off[ai] + a.up[ai], le = a.off[ai + 1];
+            const int nj = d - 1 - i;
+            unsigned bits = 0;
+            if (le - ls <= (int64_t)a.stream_max) {
+                // stream N+(S[i]); each entry looked up in S[i+1, d) (shared memory)
+                for (int64_t x0 = ls; x0 < le; x0 += 32) {
+                    const int64_t x = x0 + lane;
+                    const int32_t v = x < le ? cols[x] : INT32_MAX;
+                    if (!__any_sync(kFull, v <= smax)) break;
+                    if (v <= smax) {
+                        ++items;
+                        const int j = search_local(sS[wib], i + 1, d, v);
+                        if (j >= 0) bits |= 1u << j;
+                    }
+                }
+                bits = __reduce_or_sync(kFull, bits);
+            } else {
+                const bool f = lane > i && lane < d && search_list(cols, ls, le, sv, probes);
+                bits = __ballot_sync(kFull, f);
+                items += (lane > i && lane < d);
+            }
+            (void)nj;
+            if (lane == i) myrow = bits;
+            if (K == 3 && lane == 0) cnt += __popc(bits);
+        }
+        if (K == 4) {
+            sA[wib][lane] = myrow;
+            __syncwarp();
+            unsigned b = myrow;
+            while (b) {
+                const int j = __ffs(b) - 1;
+                b &= b - 1;
+                cnt += __popc(myrow & sA[wib][j]);
+            }
+        }
+        __syncwarp();
+    }
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(kFull, cnt, o);
+        items += __shfl_xor_sync(kFull, items, o);
+        probes += __shfl_xor_sync(kFull, probes, o);
+    }
+    if (lane == 0) {
+        if (cnt) atomicAdd(a.count, cnt);
+        if (cnt) atomicAdd(&a.stats[3], cnt);
+        if (items) atomicAdd(&a.stats[0], items);
+        if (probes) atomicAdd(&a.stats[1], (unsigned long long)probes);
+        if (sent) atomicAdd(&a.stats[4], sent);
+    }
+}
+
+// ---------------------------------------------------------------------------- d > 32
+template <int K, bool kGlobal, int NT>
+__global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
+    extern __shared__ __align__(16) int32_t csm[];
+    constexpr int NW = NT / 32;
+    __shared__ int32_t sJ[NW][32];
+    __shared__ int sRow[2];
+    __shared__ unsigned long long sRoot;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int32_t* __restrict__ cols = a.cols;
+    int32_t* S;
+    if (kGlobal) S = a.slab + (int64_t)blockIdx.x * slab_ints(a.dmax);
+    else S = csm;
+    unsigned* A = reinterpret_cast<unsigned*>(S + a.dmax);
+    unsigned long long cnt = 0, items = 0, words = 0, sent = 0;
+    unsigned probes = 0;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            sRoot = atomicAdd(a.next, 1ull);
+            sRow[0] = 0;
+            sRow[1] = 0;
+        }
+        __syncthreads();
+        const int64_t t = (int64_t)sRoot;
+        if (t >= a.n) break;
+        const int32_t u = a.roots[a.idx[t]];
+        const int64_t s0 = a.off[u] + a.up[u];
+        const int d = (int)(a.off[u + 1] - s0);
+        const int W = (d + 31) >> 5, Wp = W | 1;
+        for (int j = threadIdx.x; j < d; j += NT) S[j] = cols[s0 + j];
+        if (threadIdx.x == 0) sent += d;
+        __syncthreads();
+        const int32_t smax = S[d - 1];
+        // ---- rows A[i] (level 1 -> 2 connection tests), warps take rows dynamically
+        for (;;) {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(&sRow[0], 1);
+            i = __shfl_sync(kFull, i, 0);
+            if (i >= d) break;
+            unsigned* Ai = A + (int64_t)i * Wp;
+            const int w0 = i >> 5;
+            if (i == d - 1) {  // no j > i: an all-zero row (read by the pair phase)
+                if (K == 4 && lane == 0) Ai[w0] = 0;
+                continue;
+            }
+            const int32_t ai = S[i];
+            const int64_t ls = a.off[ai] + a.up[ai], le = a.off[ai + 1];
+            const int nj = d - 1 - i;
+            if ((le - ls) * 32 <= (int64_t)a.stream_max * nj) {
+                if (K == 4) {
+                    for (int w = w0 + lane; w < W; w += 32) Ai[w] = 0;
+                    __syncwarp();
+                }
+                for (int64_t x0 = ls; x0 < le; x0 += 32) {
+                    const int64_t x = x0 + lane;
+                    const int32_t v = x < le ? cols[x] : INT32_MAX;
+                    if (!__any_sync(kFull, v <= smax)) break;
+                    if (v <= smax) {
+                        ++items;
+                        const int j = search_local(S, i + 1, d, v);
+                        if (j >= 0) {
+                            if (K == 4) atomicOr(&Ai[j >> 5], 1u << (j & 31));
+                            else ++cnt;
+                        }
+                    }
+                }
+            } else {
+                for (int w = w0; w < W; ++w) {
+                    const int j = (w << 5) + lane;
+                    const bool live = j > i && j < d;
+                    items += live;
+                    const bool f = live && search_list(cols, ls, le, S[j], probes);
+                    const unsigned bits = __ballot_sync(kFull, f);
+                    if (K == 4) {
+                        if (lane == 0) Ai[w] = bits;
+                    } else {
+                        cnt += f;
+                    }
+                }
+            }
+        }
+        if (K == 3) continue;
+        __syncthreads();
+        // ---- level 3: for every level-2 partial result (u, S[i], S[j]) (bit j of A[i]):
+        //      |{l : A[i] bit l and A[j] bit l}| = popc over words of A[i] & A[j]
+        for (;;) {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(&sRow[1], 1);
+            i = __shfl_sync(kFull, i, 0);
+            if (i >= d - 1) break;
+            const unsigned* Ai = A + (int64_t)i * Wp;
+            int nJ = 0;
+            for (int w = i >> 5; w < W; ++w) {
+                unsigned bits = Ai[w];
+                while (bits) {
+                    const int c = __popc(bits);
+                    const int take = min(c, 32 - nJ);
+                    const bool has = (bits >> lane) & 1u;
+                    const int rank = __popc(bits & ((1u << lane) - 1u));
+                    const bool tk = has && rank < take;
+                    if (tk) sJ[wib][nJ + rank] = (w << 5) + lane;
+                    bits &= ~__ballot_sync(kFull, tk);
+                    nJ += take;
+                    if (nJ == 32) {
+                        __syncwarp();
+                        const int j = sJ[wib][lane];
+                        const unsigned* Aj = A + (int64_t)j * Wp;
+                        for (int x = j >> 5; x < W; ++x) cnt += __popc(Ai[x] & Aj[x]);
+                        words += W - (j >> 5);
+                        nJ = 0;
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane < nJ) {
+                const int j = sJ[wib][lane];
+                const unsigned* Aj = A + (int64_t)j * Wp;
+                for (int x = j >> 5; x < W; ++x) cnt += __popc(Ai[x] & Aj[x]);
+                words += W - (j >> 5);
+            }
+            __syncwarp();
+        }
+    }
+    unsigned long long pr = probes;
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(kFull, cnt, o);
+        items += __shfl_xor_sync(kFull, items, o);
+        pr += __shfl_xor_sync(kFull, pr, o);
+        words += __shfl_xor_sync(kFull, words, o);
+    }
+    if (lane == 0) {
+        if (cnt) {
+            atomicAdd(a.count, cnt);
+            atomicAdd(&a.stats[3], cnt);
+        }
+        if (items) atomicAdd(&a.stats[0], items);
+        if (pr) atomicAdd(&a.stats[1], pr);
+        if (words) atomicAdd(&a.stats[2], words);
+        if (sent) atomicAdd(&a.stats[4], sent);
+    }
+}
+
+static int64_t slab_ints_host(int dmax) {
+    const int64_t W = (dmax + 31) >> 5;
+    return dmax + dmax * (W | 1);
+}
+
+static int sm_count() {
+    int dev = 0, sms = 148;
+    GSM_CUDA(cudaGetDevice(&dev));
+    GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return sms;
+}
+
+static size_t cta_smem(int K, int dmax) {
+    const int W = (dmax + 31) >> 5;
+    return sizeof(int32_t) * ((size_t)dmax + (K == 4 ? (size_t)dmax * (W | 1) : 0));
+}
+
+// largest d whose S + A fit the opt-in shared memory of one CTA (K = 4), or S alone (K = 3)
+int clique_dsmem(int K) {
+    const char* v = getenv("GSM_CLIQUE_DSMEM");
+    const size_t lim = 200 * 1024;
+    int d = 32;
+    while (cta_smem(K, d + 32) <= lim) d += 32;
+    if (v && *v) d = std::min(d, std::max(64, atoi(v)));
+    return d;
+}
+
+static int warp_max() {  // GSM_CLIQUE_WARP=0: no warp-per-root kernel (tests)
+    const char* v = getenv("GSM_CLIQUE_WARP");
+    return (v && *v == '0') ? 0 : 32;
+}
+
+static int stream_max() {
+    const char* v = getenv("GSM_CLIQUE_STREAM");
+    return (v && *v) ? atoi(v) : 128;
+}
+
+template <int K, bool G, int NT>
+static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
+    const size_t smem = G ? 0 : cta_smem(K, a.dmax);
+    GSM_CUDA(cudaFuncSetAttribute(k_clique_cta<K, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    int per_sm = 1;
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_clique_cta<K, G, NT>, NT, smem));
+    const int64_t cap = (int64_t)sm_count() * std::max(per_sm, 1);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks, std::min<int64_t>(a.n, cap)));
+    k_clique_cta<K, G, NT><<<(unsigned)grid, NT, smem, s>>>(a);
+    GSM_LAUNCH("k_clique_cta");
+}
+
+template <int K>
+static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
+    const int64_t R = r.R;
+    const int dsmem = clique_dsmem(K);
+    DevBuf<int32_t> keys, vals, keys2, vals2, slab;
+    DevBuf<unsigned long long> bucket, sched;
+    DevBuf<int> dmax;
+    keys.ensure(R, s);
+    vals.ensure(R, s);
+    keys2.ensure(R, s);
+    vals2.ensure(R, s);
+    bucket.ensure(5, s);
+    dmax.ensure(1, s);
+    sched.ensure(5, s);
+    GSM_CUDA(cudaMemsetAsync(bucket.p, 0, sizeof(unsigned long long) * 5, s));
+    GSM_CUDA(cudaMemsetAsync(dmax.p, 0, sizeof(int), s));
+    GSM_CUDA(cudaMemsetAsync(sched.p, 0, sizeof(unsigned long long) * 5, s));
+    const int sms = sm_count();
+    k_clique_keys<<<(unsigned)std::min<int64_t>((R + 255) / 256, (int64_t)sms * 8), 256, 0, s>>>(
+        r.roots, R, r.off, r.up, K - 1, warp_max(), dsmem, keys.p, vals.p, bucket.p, dmax.p);
+    GSM_LAUNCH("k_clique_keys");
+    unsigned long long hb[5];
+    int hmax = 0;
+    GSM_CUDA(cudaMemcpyAsync(hb, bucket.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    GSM_CUDA(cudaMemcpyAsync(&hmax, dmax.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GSM_CUDA(cudaStreamSynchronize(s));
+    if (hmax == 0) return 1;
+    int end_bit = 1;
+    while (end_bit < 31 && (1 << end_bit) <= hmax) ++end_bit;
+    size_t tb = 0;
+    GSM_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys.p, keys2.p, vals.p, vals2.p, (int)R, 0,
+                                                       end_bit, s));
+    DevBuf<uint8_t> tmp;
+    tmp.ensure(tb, s);
+    GSM_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, keys.p, keys2.p, vals.p, vals2.p, (int)R, 0,
+                                                       end_bit, s));
+    int64_t launches = 1 + 1 + (end_bit + 7) / 8;  // keys, sort (histogram + passes)
+    CliqueArgs a;
+    a.roots = r.roots;
+    a.off = r.off;
+    a.cols = r.cols;
+    a.up = r.up;
+    a.stream_max = stream_max();
+    a.slab = nullptr;
+    a.count = r.count;
+    a.stats = r.stats;
+    // sorted descending: [bucket 4 | 3 | 2 | 1 | 0]
+    int64_t pos = 0;
+    for (int b = 4; b >= 0; --b) {
+        const int64_t nb = (int64_t)hb[b];
+        if (nb == 0) continue;
+        a.idx = vals2.p + pos;
+        a.n = nb;
+        a.next = sched.p + b;
+        pos += nb;
+        const int bmax = b == 4 ? hmax : b == 3 ? dsmem : b == 2 ? 512 : b == 1 ? 128 : 32;
+        a.dmax = std::min(std::min(bmax, hmax), b == 4 ? hmax : dsmem);
+        ++launches;
+        if (b == 0) {
+            const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nb + 7) / 8, (int64_t)sms * 8));
+            k_clique_warp<K><<<(unsigned)grid, 256, 0, s>>>(a);
+            GSM_LAUNCH("k_clique_warp");
+        } else if (b == 4) {
+            const int64_t blocks = std::min<int64_t>(nb, sms);
+            slab.ensure((size_t)blocks * slab_ints_host(a.dmax), s);
+            a.slab = slab.p;
+            launch_cta<K, true, 1024>(a, blocks, s);
+        } else if (b == 3) {
+            launch_cta<K, false, 1024>(a, nb, s);
+        } else {
+            launch_cta<K, false, 256>(a, nb, s);
+        }
+    }
+    return launches;
+}
+
+int64_t run_clique(const CliqueRun& r, cudaStream_t s) {
+    if (r.R <= 0) return 0;
+    return r.k == 3 ? run_clique_k<3>(r, s) : run_clique_k<4>(r, s);
+}
+
+}  // namespace gsm

@@ -114,6 +114,21 @@ void launch_tail_block(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& 
 void launch_tail(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s);
 void launch_gather_rows(const int32_t* F, int W, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s);
 
+// Clique queries K3/K4 in COUNT mode (gsm_clique.cu): per-root local bitmaps over
+// N+(u).  Adds the number of cliques (orbit representatives) to *count.
+struct CliqueRun {
+    int k;                  // 3 or 4
+    const int32_t* roots;   // level-0 frontier (new ids)
+    int64_t R;
+    const int64_t* off;
+    const int32_t* cols;
+    const int32_t* up;
+    unsigned long long* count;
+    unsigned long long* stats;  // 5: [list entries read, global probes, bitmap words, cliques, sum |N+(u)|]
+};
+int64_t run_clique(const CliqueRun& r, cudaStream_t s);  // returns kernel launches
+int clique_dsmem(int K);
+
 // Finalize ("Return ... subgraph enumeration M").
 void launch_to_query_order(const int32_t* in, int64_t N, int k, const int32_t* order, const int32_t* new2old,
                            int32_t* out, cudaStream_t s);

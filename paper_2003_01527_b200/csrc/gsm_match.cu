@@ -103,6 +103,7 @@ class Matcher {
     void process_generic(int w, const int32_t* F, int64_t R);
     void process_tail(int w, const int32_t* F, int64_t R);
     bool tail_eligible(TailArgs* ta) const;
+    bool clique_eligible() const;
     void append_output(const int32_t* rows, int64_t R);
     void finalize();
 
@@ -132,6 +133,7 @@ class Matcher {
     bool tail_ = false;        // fuse the last two positions (COUNT mode)
     TailArgs tail_args_;
     double tail_rows_ = 0;     // rows handled by the fused tail
+    bool clique_ = false;      // K3/K4 COUNT: per-root local bitmaps (gsm_clique.cu)
 };
 
 void Matcher::run() {
@@ -209,6 +211,7 @@ void Matcher::run() {
     }
 
     tail_ = tail_eligible(&tail_args_);
+    clique_ = clique_eligible();
 
     // ---- roots = C(π[0]) (level-0 frontier)
     int64_t R0 = 0;
@@ -271,6 +274,21 @@ void Matcher::run() {
     if (k_ == 1) {
         found = (uint64_t)R0;
         if (!count_mode_ && R0 > 0) append_output(lv_[1]->rows.p, R0);
+    } else if (R0 > 0 && clique_) {
+        CliqueRun cr;
+        cr.k = k_;
+        cr.roots = lv_[1]->rows.p;
+        cr.R = R0;
+        cr.off = g_.off;
+        cr.cols = g_.cols;
+        cr.up = g_.up;
+        cr.count = final_count_.p;
+        cr.stats = stats_.p + 5 * kMaxK;
+        int64_t launches = 0;
+        rec_.run(GSM_K_CLIQUE, 1, [&] { launches = run_clique(cr, s_); });
+        res_->kernel_launches += launches > 0 ? launches - 1 : 0;
+        res_->num_chunks++;
+        found = read_scalar(final_count_.p, s_);
     } else if (R0 > 0) {
         process(1, lv_[1]->rows.p, R0);
         if (count_mode_) found = read_scalar(final_count_.p, s_);
@@ -294,7 +312,14 @@ void Matcher::run() {
             res_->level_rows[w] = st[3];  // partial results with w+1 matched positions
         }
         res_->prof[GSM_K_EXPAND].alg_bytes += eb;
-        if (tail_) {
+        if (clique_) {
+            // per root: id + offset pair + up (28 B); per S(u) entry: the entry and its own
+            // offset pair + up (4 + 20 B); list entries streamed and binary-search probes (4 B)
+            const unsigned long long* st = hs.data() + 5 * kMaxK;
+            res_->prof[GSM_K_CLIQUE].alg_bytes +=
+                28.0 * (double)R0 + 24.0 * (double)st[4] + 4.0 * (double)st[0] + 4.0 * (double)st[1];
+            res_->level_work[k_ - 1] += st[0];
+        } else if (tail_) {
             const unsigned long long* st = hs.data() + 5 * kMaxK;
             const int w = k_ - 2;
             const LevelPlan& L = lplan_[w];
@@ -321,6 +346,20 @@ void Matcher::process(int w, const int32_t* F, int64_t R) {
     if (R <= 0) return;
     if (tail_ && w == k_ - 2) process_tail(w, F, R);
     else process_generic(w, F, R);
+}
+
+// Eligibility of the clique path: COUNT mode, K3 or K4, unlabeled, every position adjacent
+// to all earlier ones, and the symmetry conditions chain f(π[0]) ≺ ... ≺ f(π[k-1]).
+bool Matcher::clique_eligible() const {
+    const char* env = getenv("GSM_CLIQUE");
+    if (env && env[0] == '0') return false;
+    if (!count_mode_ || (k_ != 3 && k_ != 4) || plan_.use_labels) return false;
+    for (int i = 1; i < k_; ++i) {
+        const LevelPlan& L = lplan_[i];
+        if (plan_.backward[i] != (1u << i) - 1u) return false;
+        if (L.keyed || L.nhi != 0 || L.nlo != i) return false;
+    }
+    return true;
 }
 
 // Eligibility of the fused tail: COUNT mode; B(k-1) = B(k-2) ∪ {k-2}; π[k-1] has the

@@ -27,7 +27,7 @@ GSM_MODE_ENUMERATE = 1
 GSM_FLAG_UNIQUE = 1
 GSM_FLAG_NO_SYMMETRY = 2
 GSM_FLAG_PROFILE = 4
-KERNEL_NAMES = ["filter", "roots", "plan", "scan", "expand", "finalize", "tail"]
+KERNEL_NAMES = ["filter", "roots", "plan", "scan", "expand", "finalize", "tail", "clique"]
 
 
 class GsmError(RuntimeError):
@@ -66,7 +66,7 @@ class gsm_result(ctypes.Structure):
                 ("order", ctypes.c_int32 * MAX_K), ("candidates", ctypes.c_uint64 * MAX_K),
                 ("level_rows", ctypes.c_uint64 * MAX_K), ("level_work", ctypes.c_uint64 * MAX_K),
                 ("num_chunks", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
-                ("prof", gsm_kernel_prof * 7), ("device", ctypes.c_int32), ("symmetric", ctypes.c_int32)]
+                ("prof", gsm_kernel_prof * 8), ("device", ctypes.c_int32), ("symmetric", ctypes.c_int32)]
 
 
 class gsm_plan_info(ctypes.Structure):

@@ -156,12 +156,18 @@ def test_config4_rmat24_triangles_exact(rmat24):
     assert tot == c
 
 
-def test_config4_rmat24_k4_sampled_and_identities(rmat24):
+def test_config4_rmat24_k4_sampled_and_identities(rmat24, monkeypatch):
     w, g, G = rmat24
     q = gi.query("K4")
-    c_all, _, r = run(G, q, "count", mem_budget_bytes=w.mem_budget_bytes)
+    c_all, _, r = run(G, q, "count", mem_budget_bytes=w.mem_budget_bytes)  # clique bitmap path
     assert c_all == 24 * r.count_unique and c_all > 0
-    assert r.num_chunks > 1  # the fixed budget forces a chunked frontier
+    assert r.prof["clique"]["launches"] > 0
+    # the breadth-first path (fused tail) under the fixed budget: chunked frontier, same count
+    monkeypatch.setenv("GSM_CLIQUE", "0")
+    c_bfs, _, r2 = run(G, q, "count", mem_budget_bytes=w.mem_budget_bytes)
+    monkeypatch.delenv("GSM_CLIQUE")
+    assert r2.num_chunks > 1  # the fixed budget forces a chunked frontier
+    assert c_bfs == c_all
     roots = _root_sample(g, None, 128, 11, n_high=0)  # the plain DFS needs ~0.2 s per R-MAT-24 root
     cnt, ref = oracle.match(g, q, roots=roots)
     c, rows, _ = run(G, q, "enumerate", root_subset=roots)

@@ -142,6 +142,49 @@ def test_fused_tail_matches_generic_path(tail, monkeypatch):
         G.free()
 
 
+@pytest.fixture(scope="module")
+def dense_gnp():
+    """G(1200, 1/2): min degree > 512, so N+(u) of the lowest-ranked vertices exceeds 512
+    (the shared-memory CTA bucket above 512); exact counts from the oracle's independent
+    degree-ordered clique counters."""
+    g = gi.random_gnp(1200, 1, 2, 7)
+    return g, oracle.count_triangles(g), oracle.count_k4(g)
+
+
+@pytest.mark.parametrize("variant", ["default", "warp0", "dsmem64", "search", "stream", "off"])
+def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
+    """K3/K4 COUNT through the per-root local-bitmap kernels (gsm_clique.cu) in every
+    bucket (warp per root; CTA with shared memory; CTA with a global slab via a tiny
+    GSM_CLIQUE_DSMEM) and both row-construction strategies, against the oracle (DFS on an
+    R-MAT graph, independent clique counters on a dense G(n, p)).  "off" = the fused-tail
+    path (GSM_CLIQUE=0) on the same inputs."""
+    env = {"warp0": {"GSM_CLIQUE_WARP": "0"}, "dsmem64": {"GSM_CLIQUE_DSMEM": "64"},
+           "search": {"GSM_CLIQUE_STREAM": "0"}, "stream": {"GSM_CLIQUE_STREAM": "1000000000"},
+           "off": {"GSM_CLIQUE": "0"}}.get(variant, {})
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = gi.rmat(10, 16, seed=12)
+    G = load(g)
+    try:
+        for q in [gi.query("K3"), gi.query("K4")]:
+            cnt, _ = oracle.match(g, q, count_only=True)
+            c, _, r = run(G, q, "count")
+            assert c == cnt, (variant, q.name, c, cnt)
+            assert (r.prof["clique"]["launches"] > 0) == (variant != "off"), r.prof
+            cu, _, _ = run(G, q, "count", flags=gsm.GSM_FLAG_UNIQUE)
+            assert cu * r.automorphisms == cnt
+    finally:
+        G.free()
+    gd, T, K4 = dense_gnp
+    G = load(gd)
+    try:
+        assert run(G, gi.query("K3"), "count", flags=gsm.GSM_FLAG_UNIQUE)[0] == T, variant
+        assert run(G, gi.query("K4"), "count", flags=gsm.GSM_FLAG_UNIQUE)[0] == K4, variant
+        assert run(G, gi.query("K4"), "count")[0] == 24 * K4, variant
+    finally:
+        G.free()
+
+
 def test_ne_refinement_is_sound():
     """NE filter + refinement rounds (Alg. 1 lines 7-8): results
     identical for R = 0..3; |C(u)| non-increasing in R and never below the number of

@@ -60,6 +60,27 @@ __device__ __forceinline__ int search_local(const int32_t* S, int lo, int hi, in
     return (l < hi && S[l] == key) ? l : -1;
 }
 
+// open-addressing table of local indices into S (membership of a streamed list entry in
+// S(u) in ~1-2 shared-memory probes instead of a log2|S| binary search)
+__host__ __device__ __forceinline__ int hash_slots(int dmax) {
+    int P = 64;
+    while (P < 2 * dmax) P <<= 1;
+    return P;
+}
+
+__device__ __forceinline__ unsigned hash_of(int32_t v, int logP) {
+    return ((unsigned)v * 0x9E3779B1u) >> (32 - logP);
+}
+
+__device__ __forceinline__ int hash_find(const int32_t* H, const int32_t* S, int logP, int32_t v) {
+    const unsigned m = (1u << logP) - 1u;
+    for (unsigned h = hash_of(v, logP);; h = (h + 1) & m) {
+        const int j = H[h];
+        if (j < 0) return -1;
+        if (S[j] == v) return j;
+    }
+}
+
 __device__ __forceinline__ int slab_ints(int dmax) {
     const int W = (dmax + 31) >> 5;
     return dmax + dmax * (W | 1);
@@ -107,6 +128,8 @@ struct CliqueArgs {
     const int32_t* up;
     int32_t dmax;           // max |N+(u)| of this launch (sizes shared memory / the slab)
     int32_t stream_max;     // row construction streams N+(S[i]) when its length <= stream_max * (#j)/32
+    int32_t use_hash;       // k_clique_cta: S(u) membership by hash table (else binary search)
+    int32_t dbg;            // GSM_CLIQUE_DBG (timing experiments only; wrong counts): 1 = no level 3, 2 = no row writes
     int32_t* slab;          // kGlobal: per-CTA scratch of slab_ints(dmax) ints
     unsigned long long* next;   // dynamic root scheduler
     unsigned long long* count;  // unique cliques (atomic)
@@ -197,8 +220,9 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int32_t* __restrict__ cols = a.cols;
     int32_t* S;
+    int32_t* H = csm;  // hash_slots(dmax) local indices (-1 = empty)
     if (kGlobal) S = a.slab + (int64_t)blockIdx.x * slab_ints(a.dmax);
-    else S = csm;
+    else S = csm + (a.use_hash ? hash_slots(a.dmax) : 0);
     unsigned* A = reinterpret_cast<unsigned*>(S + a.dmax);
     unsigned long long cnt = 0, items = 0, words = 0, sent = 0;
     unsigned probes = 0;
@@ -216,9 +240,20 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
         const int64_t s0 = a.off[u] + a.up[u];
         const int d = (int)(a.off[u + 1] - s0);
         const int W = (d + 31) >> 5, Wp = W | 1;
+        int logP = 6;
+        while ((1 << logP) < 2 * d) ++logP;
+        if (a.use_hash)
+            for (int h = threadIdx.x; h < (1 << logP); h += NT) H[h] = -1;
         for (int j = threadIdx.x; j < d; j += NT) S[j] = cols[s0 + j];
         if (threadIdx.x == 0) sent += d;
         __syncthreads();
+        if (a.use_hash) {
+            const unsigned m = (1u << logP) - 1u;
+            for (int j = threadIdx.x; j < d; j += NT)
+                for (unsigned h = hash_of(S[j], logP);; h = (h + 1) & m)
+                    if (atomicCAS(&H[h], -1, j) == -1) break;
+            __syncthreads();
+        }
         const int32_t smax = S[d - 1];
         // ---- rows A[i] (level 1 -> 2 connection tests), warps take rows dynamically
         for (;;) {
@@ -246,9 +281,11 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
                     if (!__any_sync(kFull, v <= smax)) break;
                     if (v <= smax) {
                         ++items;
-                        const int j = search_local(S, i + 1, d, v);
+                        const int j = a.use_hash ? hash_find(H, S, logP, v) : search_local(S, i + 1, d, v);
                         if (j >= 0) {
-                            if (K == 4) atomicOr(&Ai[j >> 5], 1u << (j & 31));
+                            if (K == 4) {
+                                if (!(a.dbg & 2)) atomicOr(&Ai[j >> 5], 1u << (j & 31));
+                            }
                             else ++cnt;
                         }
                     }
@@ -268,7 +305,7 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
                 }
             }
         }
-        if (K == 3) continue;
+        if (K == 3 || (a.dbg & 1)) continue;
         __syncthreads();
         // ---- level 3: for every level-2 partial result (u, S[i], S[j]) (bit j of A[i]):
         //      |{l : A[i] bit l and A[j] bit l}| = popc over words of A[i] & A[j]
@@ -342,15 +379,22 @@ static int sm_count() {
     return sms;
 }
 
-static size_t cta_smem(int K, int dmax) {
+static int use_hash() {  // GSM_CLIQUE_HASH=0: binary search in S(u) instead
+    const char* v = getenv("GSM_CLIQUE_HASH");
+    return (v && *v == '0') ? 0 : 1;
+}
+
+static size_t cta_smem(int K, int dmax, bool global = false) {
     const int W = (dmax + 31) >> 5;
-    return sizeof(int32_t) * ((size_t)dmax + (K == 4 ? (size_t)dmax * (W | 1) : 0));
+    const size_t h = use_hash() ? (size_t)hash_slots(dmax) : 0;
+    if (global) return sizeof(int32_t) * h;
+    return sizeof(int32_t) * (h + (size_t)dmax + (K == 4 ? (size_t)dmax * (W | 1) : 0));
 }
 
 // largest d whose S + A fit the opt-in shared memory of one CTA (K = 4), or S alone (K = 3)
 int clique_dsmem(int K) {
     const char* v = getenv("GSM_CLIQUE_DSMEM");
-    const size_t lim = 200 * 1024;
+    const size_t lim = 220 * 1024;  // + static (row lists, counters) <= 227 KB
     int d = 32;
     while (cta_smem(K, d + 32) <= lim) d += 32;
     if (v && *v) d = std::min(d, std::max(64, atoi(v)));
@@ -369,8 +413,8 @@ static int stream_max() {
 
 template <int K, bool G, int NT>
 static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
-    const size_t smem = G ? 0 : cta_smem(K, a.dmax);
-    GSM_CUDA(cudaFuncSetAttribute(k_clique_cta<K, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    const size_t smem = cta_smem(K, a.dmax, G);
+    GSM_CUDA(cudaFuncSetAttribute(k_clique_cta<K, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     int per_sm = 1;
     GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_clique_cta<K, G, NT>, NT, smem));
     const int64_t cap = (int64_t)sm_count() * std::max(per_sm, 1);
@@ -422,6 +466,8 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
     a.cols = r.cols;
     a.up = r.up;
     a.stream_max = stream_max();
+    a.use_hash = use_hash();
+    a.dbg = getenv("GSM_CLIQUE_DBG") ? atoi(getenv("GSM_CLIQUE_DBG")) : 0;
     a.slab = nullptr;
     a.count = r.count;
     a.stats = r.stats;

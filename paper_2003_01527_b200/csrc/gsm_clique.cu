@@ -81,23 +81,20 @@ __device__ __forceinline__ int hash_find(const int32_t* H, const int32_t* S, int
     }
 }
 
-__device__ __forceinline__ int slab_ints(int dmax) {
-    const int W = (dmax + 31) >> 5;
-    return dmax + dmax * (W | 1);
-}
-
 }  // namespace
 
-// keys[r] = |N+(roots[r])| (0 if below k-1: no clique through it), vals[r] = r;
-// bucket counts (d <= wmax: warp; d > dsmem: global slab; else d <= 128, <= 512, <= dsmem)
-// and the max.  Descending keys keep every bucket contiguous in the sorted order.
+struct BucketEdges {
+    int e[6];  // |S(u)| upper edges of buckets 0..5; bucket 6 = beyond e[5] (global slab)
+};
+
+// keys[r] = |N+(roots[r])| (0 if below k-1: no clique through it), vals[r] = r; bucket
+// counts and the max.  Descending keys keep every bucket contiguous in the sorted order.
 __global__ void k_clique_keys(const int32_t* __restrict__ roots, int64_t R, const int64_t* __restrict__ off,
-                              const int32_t* __restrict__ up, int kmin, int wmax, int dsmem,
-                              int32_t* __restrict__ keys,
+                              const int32_t* __restrict__ up, int kmin, BucketEdges E, int32_t* __restrict__ keys,
                               int32_t* __restrict__ vals, unsigned long long* __restrict__ bucket, int* dmax) {
-    __shared__ unsigned long long sb[5];
+    __shared__ unsigned long long sb[7];
     __shared__ int sm;
-    if (threadIdx.x < 5) sb[threadIdx.x] = 0;
+    if (threadIdx.x < 7) sb[threadIdx.x] = 0;
     if (threadIdx.x == 0) sm = 0;
     __syncthreads();
     int lm = 0;
@@ -108,14 +105,15 @@ __global__ void k_clique_keys(const int32_t* __restrict__ roots, int64_t R, cons
         keys[r] = d;
         vals[r] = (int32_t)r;
         if (d > 0) {
-            const int b = d <= wmax ? 0 : d > dsmem ? 4 : d <= 128 ? 1 : d <= 512 ? 2 : 3;
+            int b = 0;
+            while (b < 6 && d > E.e[b]) ++b;
             atomicAdd(&sb[b], 1ull);
             lm = max(lm, d);
         }
     }
     atomicMax(&sm, lm);
     __syncthreads();
-    if (threadIdx.x < 5 && sb[threadIdx.x]) atomicAdd(&bucket[threadIdx.x], sb[threadIdx.x]);
+    if (threadIdx.x < 7 && sb[threadIdx.x]) atomicAdd(&bucket[threadIdx.x], sb[threadIdx.x]);
     if (threadIdx.x == 0 && sm) atomicMax(dmax, sm);
 }
 
@@ -130,7 +128,7 @@ struct CliqueArgs {
     int32_t stream_max;     // row construction streams N+(S[i]) when its length <= stream_max * (#j)/32
     int32_t use_hash;       // k_clique_cta: S(u) membership by hash table (else binary search)
     int32_t dbg;            // GSM_CLIQUE_DBG (timing experiments only; wrong counts): 1 = no level 3, 2 = no row writes
-    int32_t* slab;          // kGlobal: per-CTA scratch of slab_ints(dmax) ints
+    int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
     unsigned long long* next;   // dynamic root scheduler
     unsigned long long* count;  // unique cliques (atomic)
     unsigned long long* stats;  // [list entries read, global probes, bitmap words, cliques, sum |S(u)|]
@@ -210,8 +208,63 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
 }
 
 // ---------------------------------------------------------------------------- d > 32
-template <int K, bool kGlobal, int NT>
-__global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
+// Per-CTA workspace (int32 units), identical on host and device.  Shared memory always
+// holds the hash table H, the Bloom filter BL and the row-block table TB; S(u), the row
+// metadata (RL: |N+(S[i])|, RB: its start) and the bit rows A are in shared memory too,
+// or in a per-CTA global slab (kGlobal) for |S(u)| beyond what one CTA can hold.
+// Bit rows are stored triangular: row i keeps words i/32 .. W-1 only (bits <= i are 0),
+// rows of block b = i/32 have odd length (W-b)|1 (conflict-free column reads).
+__host__ __device__ inline int bloom_words(int dmax) {
+    int bits = 1024;
+    while (bits < 16 * dmax) bits <<= 1;
+    return bits >> 5;
+}
+
+__host__ __device__ inline int64_t tri_words(int d) {
+    const int W = (d + 31) >> 5;
+    int64_t t = 0;
+    for (int b = 0; b < W; ++b) t += (int64_t)min(32, d - 32 * b) * ((W - b) | 1);
+    return t;
+}
+
+struct CtaLay {
+    int64_t h, bl, tb, s, rl, rb, A;  // offsets (int32 units) in shared memory or the slab
+    int64_t smem_ints, slab_ints;
+};
+
+__host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool hash) {
+    CtaLay L;
+    int64_t o = 0, g = 0;
+    const int W = (dmax + 31) >> 5;
+    L.h = o;
+    o += hash ? hash_slots(dmax) : 0;
+    L.bl = o;
+    o += bloom_words(dmax);
+    L.tb = o;
+    o += 2 * (W + 1);
+    int64_t& q = global ? g : o;
+    q = (q + 1) & ~1LL;
+    L.s = q;
+    q += dmax;
+    L.rl = q;
+    q += dmax;
+    q = (q + 1) & ~1LL;  // int64 alignment
+    L.rb = q;
+    q += 2 * (int64_t)dmax;
+    L.A = q;
+    q += K == 4 ? tri_words(dmax) : 0;
+    q = (q + 1) & ~1LL;
+    L.smem_ints = o;
+    L.slab_ints = g;
+    return L;
+}
+
+__device__ __forceinline__ unsigned bloom_of(int32_t v, int logB) {
+    return ((unsigned)v * 0x85EBCA6Bu + 0x7F4A7C15u) >> (32 - logB);
+}
+
+template <int K, bool kGlobal, int NT, int kMinB>
+__global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     extern __shared__ __align__(16) int32_t csm[];
     constexpr int NW = NT / 32;
     __shared__ int32_t sJ[NW][32];
@@ -219,11 +272,15 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
     __shared__ unsigned long long sRoot;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int32_t* __restrict__ cols = a.cols;
-    int32_t* S;
-    int32_t* H = csm;  // hash_slots(dmax) local indices (-1 = empty)
-    if (kGlobal) S = a.slab + (int64_t)blockIdx.x * slab_ints(a.dmax);
-    else S = csm + (a.use_hash ? hash_slots(a.dmax) : 0);
-    unsigned* A = reinterpret_cast<unsigned*>(S + a.dmax);
+    const CtaLay L = cta_lay(K, a.dmax, kGlobal, a.use_hash != 0);
+    int32_t* ws = kGlobal ? a.slab + (int64_t)blockIdx.x * L.slab_ints : csm;
+    int32_t* H = csm + L.h;
+    unsigned* BL = reinterpret_cast<unsigned*>(csm + L.bl);
+    int32_t* TB = csm + L.tb;  // TB[b] = first word of row block b, TB[W + 1 + b] = its row length
+    int32_t* S = ws + L.s;
+    int32_t* RL = ws + L.rl;
+    int64_t* RB = reinterpret_cast<int64_t*>(ws + L.rb);
+    unsigned* A = reinterpret_cast<unsigned*>(ws + L.A);
     unsigned long long cnt = 0, items = 0, words = 0, sent = 0;
     unsigned probes = 0;
     for (;;) {
@@ -239,21 +296,42 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
         const int32_t u = a.roots[a.idx[t]];
         const int64_t s0 = a.off[u] + a.up[u];
         const int d = (int)(a.off[u + 1] - s0);
-        const int W = (d + 31) >> 5, Wp = W | 1;
-        int logP = 6;
+        const int W = (d + 31) >> 5;
+        int logP = 6, logB = 10;
         while ((1 << logP) < 2 * d) ++logP;
+        while ((1 << logB) < 16 * d) ++logB;
         if (a.use_hash)
             for (int h = threadIdx.x; h < (1 << logP); h += NT) H[h] = -1;
-        for (int j = threadIdx.x; j < d; j += NT) S[j] = cols[s0 + j];
+        for (int h = threadIdx.x; h < (1 << (logB - 5)); h += NT) BL[h] = 0;
+        if (K == 4 && threadIdx.x < W) {
+            int base = 0;
+            for (int b = 0; b < (int)threadIdx.x; ++b) base += 32 * ((W - b) | 1);
+            TB[threadIdx.x] = base;
+            TB[W + 1 + threadIdx.x] = (W - threadIdx.x) | 1;
+        }
+        // S(u) and, per entry, its own list N+(S[j]) (one parallel gather instead of a
+        // dependent chain per row)
+        for (int j = threadIdx.x; j < d; j += NT) {
+            const int32_t v = cols[s0 + j];
+            S[j] = v;
+            const int64_t b = a.off[v] + a.up[v];
+            RB[j] = b;
+            RL[j] = (int)(a.off[v + 1] - b);
+        }
         if (threadIdx.x == 0) sent += d;
         __syncthreads();
-        if (a.use_hash) {
+        {
             const unsigned m = (1u << logP) - 1u;
-            for (int j = threadIdx.x; j < d; j += NT)
-                for (unsigned h = hash_of(S[j], logP);; h = (h + 1) & m)
-                    if (atomicCAS(&H[h], -1, j) == -1) break;
-            __syncthreads();
+            for (int j = threadIdx.x; j < d; j += NT) {
+                const int32_t v = S[j];
+                const unsigned hb = bloom_of(v, logB);
+                atomicOr(&BL[hb >> 5], 1u << (hb & 31));
+                if (a.use_hash)
+                    for (unsigned h = hash_of(v, logP);; h = (h + 1) & m)
+                        if (atomicCAS(&H[h], -1, j) == -1) break;
+            }
         }
+        __syncthreads();
         const int32_t smax = S[d - 1];
         // ---- rows A[i] (level 1 -> 2 connection tests), warps take rows dynamically
         for (;;) {
@@ -261,16 +339,17 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
             if (lane == 0) i = atomicAdd(&sRow[0], 1);
             i = __shfl_sync(kFull, i, 0);
             if (i >= d) break;
-            unsigned* Ai = A + (int64_t)i * Wp;
             const int w0 = i >> 5;
-            if (i == d - 1) {  // no j > i: an all-zero row (read by the pair phase)
+            unsigned* Ai = A + TB[w0] + (i & 31) * TB[W + 1 + w0] - w0;  // Ai[w], w >= w0
+            if (i == d - 1) {  // no j > i: an all-zero row (read by level 3)
                 if (K == 4 && lane == 0) Ai[w0] = 0;
                 continue;
             }
-            const int32_t ai = S[i];
-            const int64_t ls = a.off[ai] + a.up[ai], le = a.off[ai + 1];
+            const int64_t ls = RB[i];
+            const int len = RL[i];
+            const int64_t le = ls + len;
             const int nj = d - 1 - i;
-            if ((le - ls) * 32 <= (int64_t)a.stream_max * nj) {
+            if ((int64_t)len * 32 <= (int64_t)a.stream_max * nj) {
                 if (K == 4) {
                     for (int w = w0 + lane; w < W; w += 32) Ai[w] = 0;
                     __syncwarp();
@@ -281,12 +360,16 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
                     if (!__any_sync(kFull, v <= smax)) break;
                     if (v <= smax) {
                         ++items;
-                        const int j = a.use_hash ? hash_find(H, S, logP, v) : search_local(S, i + 1, d, v);
-                        if (j >= 0) {
-                            if (K == 4) {
-                                if (!(a.dbg & 2)) atomicOr(&Ai[j >> 5], 1u << (j & 31));
+                        const unsigned hb = bloom_of(v, logB);
+                        if ((BL[hb >> 5] >> (hb & 31)) & 1u) {
+                            const int j = a.use_hash ? hash_find(H, S, logP, v) : search_local(S, i + 1, d, v);
+                            if (j >= 0) {
+                                if (K == 4) {
+                                    if (!(a.dbg & 2)) atomicOr(&Ai[j >> 5], 1u << (j & 31));
+                                } else {
+                                    ++cnt;
+                                }
                             }
-                            else ++cnt;
                         }
                     }
                 }
@@ -314,9 +397,10 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
             if (lane == 0) i = atomicAdd(&sRow[1], 1);
             i = __shfl_sync(kFull, i, 0);
             if (i >= d - 1) break;
-            const unsigned* Ai = A + (int64_t)i * Wp;
+            const int wi = i >> 5;
+            const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
             int nJ = 0;
-            for (int w = i >> 5; w < W; ++w) {
+            for (int w = wi; w < W; ++w) {
                 unsigned bits = Ai[w];
                 while (bits) {
                     const int c = __popc(bits);
@@ -330,9 +414,10 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
                     if (nJ == 32) {
                         __syncwarp();
                         const int j = sJ[wib][lane];
-                        const unsigned* Aj = A + (int64_t)j * Wp;
-                        for (int x = j >> 5; x < W; ++x) cnt += __popc(Ai[x] & Aj[x]);
-                        words += W - (j >> 5);
+                        const int wj = j >> 5;
+                        const unsigned* Aj = A + TB[wj] + (j & 31) * TB[W + 1 + wj] - wj;
+                        for (int x = wj; x < W; ++x) cnt += __popc(Ai[x] & Aj[x]);
+                        words += W - wj;
                         nJ = 0;
                         __syncwarp();
                     }
@@ -341,9 +426,10 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
             __syncwarp();
             if (lane < nJ) {
                 const int j = sJ[wib][lane];
-                const unsigned* Aj = A + (int64_t)j * Wp;
-                for (int x = j >> 5; x < W; ++x) cnt += __popc(Ai[x] & Aj[x]);
-                words += W - (j >> 5);
+                const int wj = j >> 5;
+                const unsigned* Aj = A + TB[wj] + (j & 31) * TB[W + 1 + wj] - wj;
+                for (int x = wj; x < W; ++x) cnt += __popc(Ai[x] & Aj[x]);
+                words += W - wj;
             }
             __syncwarp();
         }
@@ -367,11 +453,6 @@ __global__ void __launch_bounds__(NT) k_clique_cta(CliqueArgs a) {
     }
 }
 
-static int64_t slab_ints_host(int dmax) {
-    const int64_t W = (dmax + 31) >> 5;
-    return dmax + dmax * (W | 1);
-}
-
 static int sm_count() {
     int dev = 0, sms = 148;
     GSM_CUDA(cudaGetDevice(&dev));
@@ -385,18 +466,16 @@ static int use_hash() {  // GSM_CLIQUE_HASH=0: binary search in S(u) instead
 }
 
 static size_t cta_smem(int K, int dmax, bool global = false) {
-    const int W = (dmax + 31) >> 5;
-    const size_t h = use_hash() ? (size_t)hash_slots(dmax) : 0;
-    if (global) return sizeof(int32_t) * h;
-    return sizeof(int32_t) * (h + (size_t)dmax + (K == 4 ? (size_t)dmax * (W | 1) : 0));
+    return sizeof(int32_t) * (size_t)cta_lay(K, dmax, global, use_hash() != 0).smem_ints;
 }
 
-// largest d whose S + A fit the opt-in shared memory of one CTA (K = 4), or S alone (K = 3)
+constexpr size_t kSmemLim = 220 * 1024;  // dynamic; + static (row lists, counters) <= 227 KB
+
+// largest |S(u)| whose whole per-root workspace fits one CTA's shared memory
 int clique_dsmem(int K) {
     const char* v = getenv("GSM_CLIQUE_DSMEM");
-    const size_t lim = 220 * 1024;  // + static (row lists, counters) <= 227 KB
     int d = 32;
-    while (cta_smem(K, d + 32) <= lim) d += 32;
+    while (cta_smem(K, d + 32) <= kSmemLim) d += 32;
     if (v && *v) d = std::min(d, std::max(64, atoi(v)));
     return d;
 }
@@ -411,22 +490,39 @@ static int stream_max() {
     return (v && *v) ? atoi(v) : 128;
 }
 
-template <int K, bool G, int NT>
-static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
+template <int K, bool G, int NT, int MB>
+static void launch_cta_mb(CliqueArgs a, int64_t blocks, cudaStream_t s) {
     const size_t smem = cta_smem(K, a.dmax, G);
-    GSM_CUDA(cudaFuncSetAttribute(k_clique_cta<K, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    GSM_CUDA(cudaFuncSetAttribute(k_clique_cta<K, G, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLim));
     int per_sm = 1;
-    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_clique_cta<K, G, NT>, NT, smem));
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_clique_cta<K, G, NT, MB>, NT, smem));
     const int64_t cap = (int64_t)sm_count() * std::max(per_sm, 1);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(blocks, std::min<int64_t>(a.n, cap)));
-    k_clique_cta<K, G, NT><<<(unsigned)grid, NT, smem, s>>>(a);
+    k_clique_cta<K, G, NT, MB><<<(unsigned)grid, NT, smem, s>>>(a);
     GSM_LAUNCH("k_clique_cta");
 }
+
+// registers capped for 2048 resident threads per SM (GSM_CLIQUE_OCC=0: uncapped; measured
+// on R-MAT-24 K3+K4: capped 760 ms vs uncapped 1,110 ms per step — the rows are latency-bound)
+template <int K, bool G, int NT>
+static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
+    static const int occ = getenv("GSM_CLIQUE_OCC") ? atoi(getenv("GSM_CLIQUE_OCC")) : 1;
+    if (occ) launch_cta_mb<K, G, NT, 2048 / NT>(a, blocks, s);
+    else launch_cta_mb<K, G, NT, 1>(a, blocks, s);
+}
+
+// bucket edges on |S(u)|: warp kernel up to kEdge[0]; CTA kernels up to each next edge
+// (shared memory sized to the bucket's largest root); global slab beyond dsmem
+constexpr int kNB = 7;
 
 template <int K>
 static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
     const int64_t R = r.R;
     const int dsmem = clique_dsmem(K);
+    BucketEdges E;
+    const int e[kNB - 1] = {warp_max(), 128, 256, 512, 1024, dsmem};
+    for (int b = 0; b < kNB - 1; ++b) E.e[b] = std::min(e[b], dsmem);
+    E.e[0] = std::min(e[0], dsmem);
     DevBuf<int32_t> keys, vals, keys2, vals2, slab;
     DevBuf<unsigned long long> bucket, sched;
     DevBuf<int> dmax;
@@ -434,17 +530,17 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
     vals.ensure(R, s);
     keys2.ensure(R, s);
     vals2.ensure(R, s);
-    bucket.ensure(5, s);
+    bucket.ensure(kNB, s);
     dmax.ensure(1, s);
-    sched.ensure(5, s);
-    GSM_CUDA(cudaMemsetAsync(bucket.p, 0, sizeof(unsigned long long) * 5, s));
+    sched.ensure(kNB, s);
+    GSM_CUDA(cudaMemsetAsync(bucket.p, 0, sizeof(unsigned long long) * kNB, s));
     GSM_CUDA(cudaMemsetAsync(dmax.p, 0, sizeof(int), s));
-    GSM_CUDA(cudaMemsetAsync(sched.p, 0, sizeof(unsigned long long) * 5, s));
+    GSM_CUDA(cudaMemsetAsync(sched.p, 0, sizeof(unsigned long long) * kNB, s));
     const int sms = sm_count();
     k_clique_keys<<<(unsigned)std::min<int64_t>((R + 255) / 256, (int64_t)sms * 8), 256, 0, s>>>(
-        r.roots, R, r.off, r.up, K - 1, warp_max(), dsmem, keys.p, vals.p, bucket.p, dmax.p);
+        r.roots, R, r.off, r.up, K - 1, E, keys.p, vals.p, bucket.p, dmax.p);
     GSM_LAUNCH("k_clique_keys");
-    unsigned long long hb[5];
+    unsigned long long hb[kNB];
     int hmax = 0;
     GSM_CUDA(cudaMemcpyAsync(hb, bucket.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
     GSM_CUDA(cudaMemcpyAsync(&hmax, dmax.p, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -471,28 +567,31 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
     a.slab = nullptr;
     a.count = r.count;
     a.stats = r.stats;
-    // sorted descending: [bucket 4 | 3 | 2 | 1 | 0]
+    // sorted descending: [bucket kNB-1 | ... | 0]
     int64_t pos = 0;
-    for (int b = 4; b >= 0; --b) {
+    for (int b = kNB - 1; b >= 0; --b) {
         const int64_t nb = (int64_t)hb[b];
         if (nb == 0) continue;
         a.idx = vals2.p + pos;
         a.n = nb;
         a.next = sched.p + b;
+        a.slab = nullptr;
         pos += nb;
-        const int bmax = b == 4 ? hmax : b == 3 ? dsmem : b == 2 ? 512 : b == 1 ? 128 : 32;
-        a.dmax = std::min(std::min(bmax, hmax), b == 4 ? hmax : dsmem);
+        a.dmax = b == kNB - 1 ? hmax : std::min(E.e[b], hmax);
         ++launches;
         if (b == 0) {
             const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nb + 7) / 8, (int64_t)sms * 8));
             k_clique_warp<K><<<(unsigned)grid, 256, 0, s>>>(a);
             GSM_LAUNCH("k_clique_warp");
-        } else if (b == 4) {
+        } else if (b == kNB - 1) {
             const int64_t blocks = std::min<int64_t>(nb, sms);
-            slab.ensure((size_t)blocks * slab_ints_host(a.dmax), s);
+            const CtaLay L = cta_lay(K, a.dmax, true, a.use_hash != 0);
+            if (cta_smem(K, a.dmax, true) > kSmemLim)
+                fail(GSM_ERR_OUT_OF_MEMORY, "clique path: |N+(u)| too large for the per-CTA hash/Bloom tables");
+            slab.ensure((size_t)blocks * L.slab_ints, s);
             a.slab = slab.p;
             launch_cta<K, true, 1024>(a, blocks, s);
-        } else if (b == 3) {
+        } else if (a.dmax > 512) {
             launch_cta<K, false, 1024>(a, nb, s);
         } else {
             launch_cta<K, false, 256>(a, nb, s);

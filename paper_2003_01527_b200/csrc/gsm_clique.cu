@@ -267,7 +267,7 @@ template <int K, bool kGlobal, int NT, int kMinB>
 __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     extern __shared__ __align__(16) int32_t csm[];
     constexpr int NW = NT / 32;
-    __shared__ int32_t sJ[NW][32];
+    __shared__ int32_t sJ[NW][64];  // level-3 j lists / Bloom-positive queue of the row phase
     __shared__ int sRow[2];
     __shared__ unsigned long long sRoot;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -354,25 +354,49 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     for (int w = w0 + lane; w < W; w += 32) Ai[w] = 0;
                     __syncwarp();
                 }
-                for (int64_t x0 = ls; x0 < le; x0 += 32) {
-                    const int64_t x = x0 + lane;
-                    const int32_t v = x < le ? cols[x] : INT32_MAX;
-                    if (!__any_sync(kFull, v <= smax)) break;
-                    if (v <= smax) {
-                        ++items;
-                        const unsigned hb = bloom_of(v, logB);
-                        if ((BL[hb >> 5] >> (hb & 31)) & 1u) {
-                            const int j = a.use_hash ? hash_find(H, S, logP, v) : search_local(S, i + 1, d, v);
-                            if (j >= 0) {
-                                if (K == 4) {
-                                    if (!(a.dbg & 2)) atomicOr(&Ai[j >> 5], 1u << (j & 31));
-                                } else {
-                                    ++cnt;
-                                }
+                // Bloom positives are queued per warp (sJ) and looked up 32 at a time, so the
+                // hash probes run converged instead of diverging on ~20 % of the lanes
+                int nq = 0;
+                auto drain = [&](int nproc) {
+                    __syncwarp();
+                    if (lane < nproc) {
+                        const int32_t v = sJ[wib][lane];
+                        const int j = a.use_hash ? hash_find(H, S, logP, v) : search_local(S, i + 1, d, v);
+                        if (j >= 0) {
+                            if (K == 4) {
+                                if (!(a.dbg & 2)) atomicOr(&Ai[j >> 5], 1u << (j & 31));
+                            } else {
+                                ++cnt;
                             }
                         }
                     }
+                    const int32_t rest = lane + 32 < nq ? sJ[wib][lane + 32] : 0;
+                    __syncwarp();
+                    if (lane + 32 < nq) sJ[wib][lane] = rest;
+                    nq -= nproc;
+                    __syncwarp();
+                };
+                auto push = [&](int32_t v) {
+                    bool pos = v <= smax;
+                    if (pos) {
+                        ++items;
+                        const unsigned hb = bloom_of(v, logB);
+                        pos = (BL[hb >> 5] >> (hb & 31)) & 1u;
+                    }
+                    const unsigned ball = __ballot_sync(kFull, pos);
+                    if (pos) sJ[wib][nq + __popc(ball & ((1u << lane) - 1u))] = v;
+                    nq += __popc(ball);
+                    if (nq >= 32) drain(32);
+                };
+                for (int64_t x0 = ls; x0 < le; x0 += 64) {  // two loads in flight per lane
+                    const int64_t x = x0 + lane;
+                    const int32_t v0 = x < le ? cols[x] : INT32_MAX;
+                    const int32_t v1 = x + 32 < le ? cols[x + 32] : INT32_MAX;
+                    if (!__any_sync(kFull, v0 <= smax)) break;
+                    push(v0);
+                    push(v1);
                 }
+                if (nq > 0) drain(nq);
             } else {
                 for (int w = w0; w < W; ++w) {
                     const int j = (w << 5) + lane;
@@ -469,7 +493,7 @@ static size_t cta_smem(int K, int dmax, bool global = false) {
     return sizeof(int32_t) * (size_t)cta_lay(K, dmax, global, use_hash() != 0).smem_ints;
 }
 
-constexpr size_t kSmemLim = 220 * 1024;  // dynamic; + static (row lists, counters) <= 227 KB
+constexpr size_t kSmemLim = 216 * 1024;  // dynamic; + static (8 KB queues, counters) <= 227 KB
 
 // largest |S(u)| whose whole per-root workspace fits one CTA's shared memory
 int clique_dsmem(int K) {

@@ -60,25 +60,33 @@ __device__ __forceinline__ int search_local(const int32_t* S, int lo, int hi, in
     return (l < hi && S[l] == key) ? l : -1;
 }
 
-// open-addressing table of local indices into S (membership of a streamed list entry in
-// S(u) in ~1-2 shared-memory probes instead of a log2|S| binary search)
-__host__ __device__ __forceinline__ int hash_slots(int dmax) {
-    int P = 64;
-    while (P < 2 * dmax) P <<= 1;
-    return P;
+// Two-table cuckoo hash of S(u): vertex id -> local index.  Entry = id << 32 | index
+// (all ones = empty).  A lookup is exactly two shared-memory probes, branch-free, so the
+// 32 lanes of a streaming step stay converged.  Tables: 2 x P entries, P = 1.25 d rounded
+// up to 32 (load <= 0.4); a 32-bit hash is mapped to [0, P) by a multiply-high.
+__host__ __device__ __forceinline__ int cuckoo_slots(int dmax) {  // P
+    return ((dmax + dmax / 4 + 31) / 32) * 32 + 32;
 }
 
-__device__ __forceinline__ unsigned hash_of(int32_t v, int logP) {
-    return ((unsigned)v * 0x9E3779B1u) >> (32 - logP);
+__device__ __forceinline__ unsigned ck_h0(int32_t v, unsigned P, unsigned seed) {
+    return __umulhi((unsigned)v * (0x9E3779B1u + 2u * seed), P);
 }
 
-__device__ __forceinline__ int hash_find(const int32_t* H, const int32_t* S, int logP, int32_t v) {
-    const unsigned m = (1u << logP) - 1u;
-    for (unsigned h = hash_of(v, logP);; h = (h + 1) & m) {
-        const int j = H[h];
-        if (j < 0) return -1;
-        if (S[j] == v) return j;
-    }
+__device__ __forceinline__ unsigned ck_h1(int32_t v, unsigned P, unsigned seed) {
+    unsigned x = (unsigned)v ^ (0x5BD1E995u + seed);
+    x *= 0x85EBCA6Bu;
+    x ^= x >> 13;
+    x *= 0xC2B2AE35u;
+    return __umulhi(x, P);
+}
+
+// local index of v in S(u), or -1
+__device__ __forceinline__ int ck_find(const unsigned long long* T, unsigned P, unsigned seed, int32_t v) {
+    const unsigned long long e0 = T[ck_h0(v, P, seed)];
+    const unsigned long long e1 = T[P + ck_h1(v, P, seed)];
+    const bool m0 = (int32_t)(e0 >> 32) == v;
+    const bool m1 = (int32_t)(e1 >> 32) == v;
+    return m0 ? (int)(unsigned)e0 : (m1 ? (int)(unsigned)e1 : -1);
 }
 
 }  // namespace
@@ -126,7 +134,7 @@ struct CliqueArgs {
     const int32_t* up;
     int32_t dmax;           // max |N+(u)| of this launch (sizes shared memory / the slab)
     int32_t stream_max;     // row construction streams N+(S[i]) when its length <= stream_max * (#j)/32
-    int32_t use_hash;       // k_clique_cta: S(u) membership by hash table (else binary search)
+    int32_t use_hash;       // k_clique_cta: cuckoo table of S(u) (0: rows by binary search only)
     int32_t dbg;            // GSM_CLIQUE_DBG (timing experiments only; wrong counts): 1 = no level 3, 2 = no row writes
     int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
     unsigned long long* next;   // dynamic root scheduler
@@ -209,17 +217,11 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
 
 // ---------------------------------------------------------------------------- d > 32
 // Per-CTA workspace (int32 units), identical on host and device.  Shared memory always
-// holds the hash table H, the Bloom filter BL and the row-block table TB; S(u), the row
+// holds the cuckoo table T and the row-block table TB; S(u), the row
 // metadata (RL: |N+(S[i])|, RB: its start) and the bit rows A are in shared memory too,
 // or in a per-CTA global slab (kGlobal) for |S(u)| beyond what one CTA can hold.
 // Bit rows are stored triangular: row i keeps words i/32 .. W-1 only (bits <= i are 0),
 // rows of block b = i/32 have odd length (W-b)|1 (conflict-free column reads).
-__host__ __device__ inline int bloom_words(int dmax) {
-    int bits = 1024;
-    while (bits < 16 * dmax) bits <<= 1;
-    return bits >> 5;
-}
-
 __host__ __device__ inline int64_t tri_words(int d) {
     const int W = (d + 31) >> 5;
     int64_t t = 0;
@@ -228,7 +230,7 @@ __host__ __device__ inline int64_t tri_words(int d) {
 }
 
 struct CtaLay {
-    int64_t h, bl, tb, s, rl, rb, A;  // offsets (int32 units) in shared memory or the slab
+    int64_t h, tb, s, rl, rb, A;  // offsets (int32 units) in shared memory or the slab
     int64_t smem_ints, slab_ints;
 };
 
@@ -236,10 +238,8 @@ __host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool has
     CtaLay L;
     int64_t o = 0, g = 0;
     const int W = (dmax + 31) >> 5;
-    L.h = o;
-    o += hash ? hash_slots(dmax) : 0;
-    L.bl = o;
-    o += bloom_words(dmax);
+    L.h = o;  // 8-byte aligned (offset 0)
+    o += hash ? 4 * (int64_t)cuckoo_slots(dmax) : 0;
     L.tb = o;
     o += 2 * (W + 1);
     int64_t& q = global ? g : o;
@@ -259,10 +259,6 @@ __host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool has
     return L;
 }
 
-__device__ __forceinline__ unsigned bloom_of(int32_t v, int logB) {
-    return ((unsigned)v * 0x85EBCA6Bu + 0x7F4A7C15u) >> (32 - logB);
-}
-
 template <int K, bool kGlobal, int NT, int kMinB>
 __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     extern __shared__ __align__(16) int32_t csm[];
@@ -274,8 +270,8 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     const int32_t* __restrict__ cols = a.cols;
     const CtaLay L = cta_lay(K, a.dmax, kGlobal, a.use_hash != 0);
     int32_t* ws = kGlobal ? a.slab + (int64_t)blockIdx.x * L.slab_ints : csm;
-    int32_t* H = csm + L.h;
-    unsigned* BL = reinterpret_cast<unsigned*>(csm + L.bl);
+    unsigned long long* T = reinterpret_cast<unsigned long long*>(csm + L.h);
+    __shared__ int sFail;
     int32_t* TB = csm + L.tb;  // TB[b] = first word of row block b, TB[W + 1 + b] = its row length
     int32_t* S = ws + L.s;
     int32_t* RL = ws + L.rl;
@@ -297,12 +293,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         const int64_t s0 = a.off[u] + a.up[u];
         const int d = (int)(a.off[u + 1] - s0);
         const int W = (d + 31) >> 5;
-        int logP = 6, logB = 10;
-        while ((1 << logP) < 2 * d) ++logP;
-        while ((1 << logB) < 16 * d) ++logB;
-        if (a.use_hash)
-            for (int h = threadIdx.x; h < (1 << logP); h += NT) H[h] = -1;
-        for (int h = threadIdx.x; h < (1 << (logB - 5)); h += NT) BL[h] = 0;
+        const unsigned P = cuckoo_slots(d);
         if (K == 4 && threadIdx.x < W) {
             int base = 0;
             for (int b = 0; b < (int)threadIdx.x; ++b) base += 32 * ((W - b) | 1);
@@ -319,17 +310,34 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             RL[j] = (int)(a.off[v + 1] - b);
         }
         if (threadIdx.x == 0) sent += d;
-        __syncthreads();
-        {
-            const unsigned m = (1u << logP) - 1u;
-            for (int j = threadIdx.x; j < d; j += NT) {
-                const int32_t v = S[j];
-                const unsigned hb = bloom_of(v, logB);
-                atomicOr(&BL[hb >> 5], 1u << (hb & 31));
-                if (a.use_hash)
-                    for (unsigned h = hash_of(v, logP);; h = (h + 1) & m)
-                        if (atomicCAS(&H[h], -1, j) == -1) break;
+        // cuckoo build (a failed build — an eviction cycle — retries with a new seed; after
+        // 4 failures the root's rows all take the binary-search strategy)
+        unsigned seed = 0;
+        bool use_ck = a.use_hash != 0;
+        for (; use_ck; ++seed) {
+            if (seed == 4) {
+                use_ck = false;
+                break;
             }
+            for (int h = threadIdx.x; h < 2 * (int)P; h += NT) T[h] = ~0ull;
+            if (threadIdx.x == 0) sFail = 0;
+            __syncthreads();
+            for (int j = threadIdx.x; j < d; j += NT) {
+                unsigned long long e = ((unsigned long long)(unsigned)cols[s0 + j] << 32) | (unsigned)j;
+                int tbl = 0;
+                int it = 0;
+                for (; it < 64; ++it) {
+                    const int32_t key = (int32_t)(e >> 32);
+                    const unsigned slot = tbl ? P + ck_h1(key, P, seed) : ck_h0(key, P, seed);
+                    e = atomicExch(&T[slot], e);
+                    if (e == ~0ull) break;
+                    tbl ^= 1;
+                }
+                if (it == 64) sFail = 1;
+            }
+            __syncthreads();
+            if (!sFail) break;
+            __syncthreads();
         }
         __syncthreads();
         const int32_t smax = S[d - 1];
@@ -349,54 +357,30 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             const int len = RL[i];
             const int64_t le = ls + len;
             const int nj = d - 1 - i;
-            if ((int64_t)len * 32 <= (int64_t)a.stream_max * nj) {
+            // streaming needs the cuckoo table; without it (GSM_CLIQUE_HASH=0, or 4 failed
+            // builds) every row takes the binary-search strategy
+            if (use_ck && (int64_t)len * 32 <= (int64_t)a.stream_max * nj) {
                 if (K == 4) {
                     for (int w = w0 + lane; w < W; w += 32) Ai[w] = 0;
                     __syncwarp();
                 }
-                // Bloom positives are queued per warp (sJ) and looked up 32 at a time, so the
-                // hash probes run converged instead of diverging on ~20 % of the lanes
-                int nq = 0;
-                auto drain = [&](int nproc) {
-                    __syncwarp();
-                    if (lane < nproc) {
-                        const int32_t v = sJ[wib][lane];
-                        const int j = a.use_hash ? hash_find(H, S, logP, v) : search_local(S, i + 1, d, v);
-                        if (j >= 0) {
-                            if (K == 4) {
-                                if (!(a.dbg & 2)) atomicOr(&Ai[j >> 5], 1u << (j & 31));
-                            } else {
-                                ++cnt;
-                            }
-                        }
-                    }
-                    const int32_t rest = lane + 32 < nq ? sJ[wib][lane + 32] : 0;
-                    __syncwarp();
-                    if (lane + 32 < nq) sJ[wib][lane] = rest;
-                    nq -= nproc;
-                    __syncwarp();
-                };
-                auto push = [&](int32_t v) {
-                    bool pos = v <= smax;
-                    if (pos) {
-                        ++items;
-                        const unsigned hb = bloom_of(v, logB);
-                        pos = (BL[hb >> 5] >> (hb & 31)) & 1u;
-                    }
-                    const unsigned ball = __ballot_sync(kFull, pos);
-                    if (pos) sJ[wib][nq + __popc(ball & ((1u << lane) - 1u))] = v;
-                    nq += __popc(ball);
-                    if (nq >= 32) drain(32);
-                };
                 for (int64_t x0 = ls; x0 < le; x0 += 64) {  // two loads in flight per lane
                     const int64_t x = x0 + lane;
                     const int32_t v0 = x < le ? cols[x] : INT32_MAX;
                     const int32_t v1 = x + 32 < le ? cols[x + 32] : INT32_MAX;
                     if (!__any_sync(kFull, v0 <= smax)) break;
-                    push(v0);
-                    push(v1);
+                    items += (v0 <= smax) + (v1 <= smax);
+                    const int j0 = ck_find(T, P, seed, v0);
+                    const int j1 = ck_find(T, P, seed, v1);
+                    if (K == 4) {
+                        if (!(a.dbg & 2)) {
+                            if (j0 >= 0) atomicOr(&Ai[j0 >> 5], 1u << (j0 & 31));
+                            if (j1 >= 0) atomicOr(&Ai[j1 >> 5], 1u << (j1 & 31));
+                        }
+                    } else {
+                        cnt += (j0 >= 0) + (j1 >= 0);
+                    }
                 }
-                if (nq > 0) drain(nq);
             } else {
                 for (int w = w0; w < W; ++w) {
                     const int j = (w << 5) + lane;
@@ -416,46 +400,52 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         __syncthreads();
         // ---- level 3: for every level-2 partial result (u, S[i], S[j]) (bit j of A[i]):
         //      |{l : A[i] bit l and A[j] bit l}| = popc over words of A[i] & A[j]
-        for (;;) {
-            int i = 0;
-            if (lane == 0) i = atomicAdd(&sRow[1], 1);
-            i = __shfl_sync(kFull, i, 0);
-            if (i >= d - 1) break;
-            const int wi = i >> 5;
-            const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
+        // (i, j) pairs are queued per warp across rows (sJ[.][0..31] = j, [32..63] = i) and
+        // processed 32 at a time, one pair per lane — rows with few bits do not leave lanes idle
+        {
             int nJ = 0;
-            for (int w = wi; w < W; ++w) {
-                unsigned bits = Ai[w];
-                while (bits) {
-                    const int c = __popc(bits);
-                    const int take = min(c, 32 - nJ);
-                    const bool has = (bits >> lane) & 1u;
-                    const int rank = __popc(bits & ((1u << lane) - 1u));
-                    const bool tk = has && rank < take;
-                    if (tk) sJ[wib][nJ + rank] = (w << 5) + lane;
-                    bits &= ~__ballot_sync(kFull, tk);
-                    nJ += take;
-                    if (nJ == 32) {
-                        __syncwarp();
-                        const int j = sJ[wib][lane];
-                        const int wj = j >> 5;
-                        const unsigned* Aj = A + TB[wj] + (j & 31) * TB[W + 1 + wj] - wj;
-                        for (int x = wj; x < W; ++x) cnt += __popc(Ai[x] & Aj[x]);
-                        words += W - wj;
-                        nJ = 0;
-                        __syncwarp();
+            auto flush = [&](int np) {
+                __syncwarp();
+                if (lane < np) {
+                    const int j = sJ[wib][lane], i = sJ[wib][32 + lane];
+                    const int wi = i >> 5, wj = j >> 5;
+                    const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
+                    const unsigned* Aj = A + TB[wj] + (j & 31) * TB[W + 1 + wj] - wj;
+                    unsigned c = 0;
+                    for (int x = wj; x < W; ++x) c += __popc(Ai[x] & Aj[x]);
+                    cnt += c;
+                    words += W - wj;
+                }
+                __syncwarp();
+            };
+            for (;;) {
+                int i = 0;
+                if (lane == 0) i = atomicAdd(&sRow[1], 1);
+                i = __shfl_sync(kFull, i, 0);
+                if (i >= d - 1) break;
+                const int wi = i >> 5;
+                const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
+                for (int w = wi; w < W; ++w) {
+                    unsigned bits = Ai[w];
+                    while (bits) {
+                        const int take = min(__popc(bits), 32 - nJ);
+                        const bool has = (bits >> lane) & 1u;
+                        const int rank = __popc(bits & ((1u << lane) - 1u));
+                        const bool tk = has && rank < take;
+                        if (tk) {
+                            sJ[wib][nJ + rank] = (w << 5) + lane;
+                            sJ[wib][32 + nJ + rank] = i;
+                        }
+                        bits &= ~__ballot_sync(kFull, tk);
+                        nJ += take;
+                        if (nJ == 32) {
+                            flush(32);
+                            nJ = 0;
+                        }
                     }
                 }
             }
-            __syncwarp();
-            if (lane < nJ) {
-                const int j = sJ[wib][lane];
-                const int wj = j >> 5;
-                const unsigned* Aj = A + TB[wj] + (j & 31) * TB[W + 1 + wj] - wj;
-                for (int x = wj; x < W; ++x) cnt += __popc(Ai[x] & Aj[x]);
-                words += W - wj;
-            }
-            __syncwarp();
+            if (nJ > 0) flush(nJ);
         }
     }
     unsigned long long pr = probes;
@@ -484,12 +474,12 @@ static int sm_count() {
     return sms;
 }
 
-static int use_hash() {  // GSM_CLIQUE_HASH=0: binary search in S(u) instead
+static int use_hash() {  // GSM_CLIQUE_HASH=0: no cuckoo table (every row by binary search; tests)
     const char* v = getenv("GSM_CLIQUE_HASH");
     return (v && *v == '0') ? 0 : 1;
 }
 
-static size_t cta_smem(int K, int dmax, bool global = false) {
+static size_t cta_smem(int K, int dmax, bool global) {
     return sizeof(int32_t) * (size_t)cta_lay(K, dmax, global, use_hash() != 0).smem_ints;
 }
 
@@ -499,7 +489,7 @@ constexpr size_t kSmemLim = 216 * 1024;  // dynamic; + static (8 KB queues, coun
 int clique_dsmem(int K) {
     const char* v = getenv("GSM_CLIQUE_DSMEM");
     int d = 32;
-    while (cta_smem(K, d + 32) <= kSmemLim) d += 32;
+    while (cta_smem(K, d + 32, false) <= kSmemLim) d += 32;
     if (v && *v) d = std::min(d, std::max(64, atoi(v)));
     return d;
 }
@@ -544,7 +534,8 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
     const int64_t R = r.R;
     const int dsmem = clique_dsmem(K);
     BucketEdges E;
-    const int e[kNB - 1] = {warp_max(), 128, 256, 512, 1024, dsmem};
+    // K4: 960 keeps two 1,024-thread CTAs (2 x 105 KB) resident per SM
+    const int e[kNB - 1] = {warp_max(), 128, 256, 512, K == 4 ? 960 : 1024, dsmem};
     for (int b = 0; b < kNB - 1; ++b) E.e[b] = std::min(e[b], dsmem);
     E.e[0] = std::min(e[0], dsmem);
     DevBuf<int32_t> keys, vals, keys2, vals2, slab;

@@ -151,7 +151,7 @@ def dense_gnp():
     return g, oracle.count_triangles(g), oracle.count_k4(g)
 
 
-@pytest.mark.parametrize("variant", ["default", "warp0", "dsmem64", "search", "stream", "off"])
+@pytest.mark.parametrize("variant", ["default", "warp0", "dsmem64", "search", "stream", "nohash", "off"])
 def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
     """K3/K4 COUNT through the per-root local-bitmap kernels (gsm_clique.cu) in every
     bucket (warp per root; CTA with shared memory; CTA with a global slab via a tiny
@@ -160,6 +160,7 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
     path (GSM_CLIQUE=0) on the same inputs."""
     env = {"warp0": {"GSM_CLIQUE_WARP": "0"}, "dsmem64": {"GSM_CLIQUE_DSMEM": "64"},
            "search": {"GSM_CLIQUE_STREAM": "0"}, "stream": {"GSM_CLIQUE_STREAM": "1000000000"},
+           "nohash": {"GSM_CLIQUE_HASH": "0"},
            "off": {"GSM_CLIQUE": "0"}}.get(variant, {})
     for k, v in env.items():
         monkeypatch.setenv(k, v)

@@ -1,5 +1,5 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -k "clique" -x -q > gpurun_out/t_clique4.log 2>&1; echo rc=$? >> gpurun_out/t_clique4.log
+# source-level ncu captures of the clique kernels on R-MAT-24 (K3 and K4, the (512,1024] bucket)
 B="python bench.py --workload rmat24 --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches2_rmat24.csv $B > /dev/null 2>&1
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_clique_cta|k_clique_warp" -c 14 -o gpurun_out/full2_rmat24 $B > gpurun_out/ncu_full2.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_clique_cta --launch-skip 1 -c 1 -o gpurun_out/k3b4 $B > gpurun_out/ncu_k3b4.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_clique_cta --launch-skip 7 -c 1 -o gpurun_out/k4b4 $B > gpurun_out/ncu_k4b4.log 2>&1
 echo done

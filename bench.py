@@ -149,23 +149,21 @@ KERNELS_OF = {"expand": ["k_expand", "k_count_walk"], "tail": ["k_tail", "k_tail
               "plan": ["k_plan_rows"], "roots": ["k_root_count", "k_root_write"]}
 
 
-def ncu_traffic(workload: str, kind: str):
-    """DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum) of the kernel of
-    this kind with the largest captured time, from profiles/ncu_summary.json (or None)."""
+def ncu_traffic(workload: str, kind: str, launches_per_step: float):
+    """DRAM bytes (ncu dram__bytes_read.sum + dram__bytes_write.sum) per recorder launch of this
+    kind: the bytes of all its kernels in the one-step capture (profiles/ncu_summary.json, written
+    by tools/ncu_summary.py metrics from `bench.py --steps 1 --warmup 0` under ncu) divided by
+    the recorder launches per step — the unit `alg_bytes_per_launch` is in.  (None if absent.)"""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         d = json.load(open(path)).get(workload, {})
     except (OSError, ValueError):
         return None, None
-    best = None
-    for name in KERNELS_OF.get(kind, []):
-        e = d.get(name)
-        if not e or e.get("dram_bytes_per_launch") is None:
-            continue
-        w = e.get("duration_s_per_launch_ncu", 0) * e.get("launches_measured", 1)
-        if best is None or w > best[0]:
-            best = (w, name, e["dram_bytes_per_launch"])
-    return (None, None) if best is None else (best[2], best[1])
+    names = [n for n in KERNELS_OF.get(kind, []) if d.get(n, {}).get("dram_bytes_total_in_capture") is not None]
+    if not names or not launches_per_step:
+        return None, None
+    tot = sum(d[n]["dram_bytes_total_in_capture"] for n in names)
+    return tot / launches_per_step, "+".join(names)
 
 
 # ----------------------------------------------------------------------------- oracle baseline
@@ -377,11 +375,12 @@ def run_ours(args, world, rank, local, dist):
     kp = prof_tot.get(dom, ex)
     achieved = (kp["alg_bytes"] / (kp["ms"] / 1e3)) / 1e9 if kp["ms"] > 0 else None
     peak = peaks.get("hbm_gbs")
-    traffic, traffic_kernel = ncu_traffic(args.workload, dom)
+    traffic, traffic_kernel = ncu_traffic(args.workload, dom, kp["launches"] / args.steps)
     roof = {"kernel": f"k_{dom}", "bound": "hbm", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if (achieved and peak) else None,
             "traffic": traffic, "traffic_kernel": traffic_kernel,
-            "traffic_source": "profiles/ncu_summary.json (ncu dram__bytes_read.sum+dram__bytes_write.sum per launch)",
+            "traffic_source": "profiles/ncu_summary.json: ncu dram__bytes_read.sum+dram__bytes_write.sum of all "
+                              "kernels of this kind in a one-step capture / recorder launches per step",
             "peak_source": peaks.get("_source", "absent"),
             "launches_per_step": kp["launches"] / args.steps,
             "kernel_ms_per_step": kp["ms"] / args.steps,

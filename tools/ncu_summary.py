@@ -156,7 +156,7 @@ def metrics(csvpath, workload):
         e = summ.setdefault(name, {})
         e.update({"launches_measured": n, "dram_read_per_launch": rd_, "dram_write_per_launch": wr_,
                   "dram_bytes_per_launch": rd_ + wr_, "duration_s_per_launch_ncu": dur,
-                  "source": os.path.basename(csvpath)})
+                  "dram_bytes_total_in_capture": (rd_ + wr_) * n, "source": os.path.basename(csvpath)})
     allp[workload] = summ
     json.dump(allp, open(path, "w"), indent=1, sort_keys=True)
     print(json.dumps(summ, indent=1))

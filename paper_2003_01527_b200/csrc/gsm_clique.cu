@@ -606,10 +606,22 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
             slab.ensure((size_t)blocks * L.slab_ints, s);
             a.slab = slab.p;
             launch_cta<K, true, 1024>(a, blocks, s);
-        } else if (a.dmax > 512) {
-            launch_cta<K, false, 1024>(a, nb, s);
         } else {
-            launch_cta<K, false, 256>(a, nb, s);
+            // CTA size with the most resident warps per SM for this bucket's shared memory
+            // (ties -> smaller CTAs: finer-grained root scheduling)
+            const size_t sm = cta_smem(K, a.dmax, false);
+            int best = 256, bestw = -1;
+            for (int nt : {256, 512, 1024}) {
+                const size_t per = sm + sizeof(int32_t) * 64 * (nt / 32) + 64 + 1024;  // + static + reserved
+                const int ctas = std::min<int>(2048 / nt, (int)((228 * 1024) / per));
+                if (ctas * nt / 32 > bestw) {
+                    bestw = ctas * nt / 32;
+                    best = nt;
+                }
+            }
+            if (best == 256) launch_cta<K, false, 256>(a, nb, s);
+            else if (best == 512) launch_cta<K, false, 512>(a, nb, s);
+            else launch_cta<K, false, 1024>(a, nb, s);
         }
     }
     return launches;

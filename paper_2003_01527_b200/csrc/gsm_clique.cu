@@ -92,7 +92,7 @@ __device__ __forceinline__ int ck_find(const unsigned long long* T, unsigned P, 
 }  // namespace
 
 struct BucketEdges {
-    int e[6];  // |S(u)| upper edges of buckets 0..5; bucket 6 = beyond e[5] (global slab)
+    int e[7];  // |S(u)| upper edges of buckets 0..6 (6 = global slab); bucket 7 = beyond e[6]
 };
 
 // keys[r] = |N+(roots[r])| (0 if below k-1: no clique through it), vals[r] = r; bucket
@@ -100,12 +100,12 @@ struct BucketEdges {
 __global__ void k_clique_keys(const int32_t* __restrict__ roots, int64_t R, const int64_t* __restrict__ off,
                               const int32_t* __restrict__ up, int kmin, BucketEdges E, int32_t* __restrict__ keys,
                               int32_t* __restrict__ vals, unsigned long long* __restrict__ bucket, int* dmax) {
-    __shared__ unsigned long long sb[7];
-    __shared__ int sm;
-    if (threadIdx.x < 7) sb[threadIdx.x] = 0;
-    if (threadIdx.x == 0) sm = 0;
+    __shared__ unsigned long long sb[8];
+    __shared__ int sm, small;
+    if (threadIdx.x < 8) sb[threadIdx.x] = 0;
+    if (threadIdx.x == 0) sm = small = 0;
     __syncthreads();
-    int lm = 0;
+    int lm = 0, lall = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
         const int32_t u = roots[r];
         int d = (int)(off[u + 1] - off[u] - up[u]);
@@ -114,15 +114,18 @@ __global__ void k_clique_keys(const int32_t* __restrict__ roots, int64_t R, cons
         vals[r] = (int32_t)r;
         if (d > 0) {
             int b = 0;
-            while (b < 6 && d > E.e[b]) ++b;
+            while (b < 7 && d > E.e[b]) ++b;
             atomicAdd(&sb[b], 1ull);
-            lm = max(lm, d);
+            if (b < 7) lm = max(lm, d);  // max over the roots this path processes
+            lall = max(lall, d);
         }
     }
     atomicMax(&sm, lm);
+    atomicMax(&small, lall);
     __syncthreads();
-    if (threadIdx.x < 7 && sb[threadIdx.x]) atomicAdd(&bucket[threadIdx.x], sb[threadIdx.x]);
+    if (threadIdx.x < 8 && sb[threadIdx.x]) atomicAdd(&bucket[threadIdx.x], sb[threadIdx.x]);
     if (threadIdx.x == 0 && sm) atomicMax(dmax, sm);
+    if (threadIdx.x == 0 && small) atomicMax(dmax + 1, small);
 }
 
 struct CliqueArgs {
@@ -527,17 +530,35 @@ static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
 
 // bucket edges on |S(u)|: warp kernel up to kEdge[0]; CTA kernels up to each next edge
 // (shared memory sized to the bucket's largest root); global slab beyond dsmem
-constexpr int kNB = 7;
+constexpr int kNB = 8;  // 0 warp, 1-5 shared memory, 6 global slab, 7 handed back
+
+__global__ void k_gather_roots(const int32_t* __restrict__ roots, const int32_t* __restrict__ idx, int64_t n,
+                               int32_t* __restrict__ out) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = roots[idx[t]];
+}
+
+// largest |S(u)| the global-slab kernel takes: its cuckoo table and block table must fit
+// shared memory, and 148 slabs must stay within ~4 GB (GSM_CLIQUE_DMAX lowers it: tests)
+static int clique_dglob(int K) {
+    int d = 1024;
+    while (cta_smem(K, d + 256, true) <= kSmemLim &&
+           (double)cta_lay(K, d + 256, true, true).slab_ints * 4.0 * 148 <= 4e9)
+        d += 256;
+    const char* v = getenv("GSM_CLIQUE_DMAX");
+    if (v && *v) d = std::min(d, std::max(8, atoi(v)));
+    return d;
+}
 
 template <int K>
-static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
+static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     const int64_t R = r.R;
     const int dsmem = clique_dsmem(K);
     BucketEdges E;
     // K4: 960 keeps two 1,024-thread CTAs (2 x 105 KB) resident per SM
-    const int e[kNB - 1] = {warp_max(), 128, 256, 512, K == 4 ? 960 : 1024, dsmem};
-    for (int b = 0; b < kNB - 1; ++b) E.e[b] = std::min(e[b], dsmem);
-    E.e[0] = std::min(e[0], dsmem);
+    const int dglob = clique_dglob(K);
+    const int e[kNB - 1] = {warp_max(), 128, 256, 512, K == 4 ? 960 : 1024, dsmem, std::max(dsmem, dglob)};
+    for (int b = 0; b < kNB - 1; ++b) E.e[b] = std::min(e[b], dglob);
     DevBuf<int32_t> keys, vals, keys2, vals2, slab;
     DevBuf<unsigned long long> bucket, sched;
     DevBuf<int> dmax;
@@ -546,23 +567,25 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
     keys2.ensure(R, s);
     vals2.ensure(R, s);
     bucket.ensure(kNB, s);
-    dmax.ensure(1, s);
+    dmax.ensure(2, s);
     sched.ensure(kNB, s);
     GSM_CUDA(cudaMemsetAsync(bucket.p, 0, sizeof(unsigned long long) * kNB, s));
-    GSM_CUDA(cudaMemsetAsync(dmax.p, 0, sizeof(int), s));
+    GSM_CUDA(cudaMemsetAsync(dmax.p, 0, 2 * sizeof(int), s));
     GSM_CUDA(cudaMemsetAsync(sched.p, 0, sizeof(unsigned long long) * kNB, s));
     const int sms = sm_count();
     k_clique_keys<<<(unsigned)std::min<int64_t>((R + 255) / 256, (int64_t)sms * 8), 256, 0, s>>>(
         r.roots, R, r.off, r.up, K - 1, E, keys.p, vals.p, bucket.p, dmax.p);
     GSM_LAUNCH("k_clique_keys");
     unsigned long long hb[kNB];
-    int hmax = 0;
+    int hm[2] = {0, 0};
     GSM_CUDA(cudaMemcpyAsync(hb, bucket.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
-    GSM_CUDA(cudaMemcpyAsync(&hmax, dmax.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GSM_CUDA(cudaMemcpyAsync(hm, dmax.p, sizeof(hm), cudaMemcpyDeviceToHost, s));
     GSM_CUDA(cudaStreamSynchronize(s));
-    if (hmax == 0) return 1;
+    const int hmax = hm[0];  // largest |S(u)| processed here; hm[1] = largest overall
+    r.n_over = (int64_t)hb[kNB - 1];
+    if (hm[1] == 0) return 1;
     int end_bit = 1;
-    while (end_bit < 31 && (1 << end_bit) <= hmax) ++end_bit;
+    while (end_bit < 31 && (1 << end_bit) <= hm[1]) ++end_bit;
     size_t tb = 0;
     GSM_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys.p, keys2.p, vals.p, vals2.p, (int)R, 0,
                                                        end_bit, s));
@@ -582,9 +605,16 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
     a.slab = nullptr;
     a.count = r.count;
     a.stats = r.stats;
-    // sorted descending: [bucket kNB-1 | ... | 0]
+    // sorted descending: [bucket kNB-1 (handed back) | kNB-2 | ... | 0]
     int64_t pos = 0;
-    for (int b = kNB - 1; b >= 0; --b) {
+    if (r.n_over > 0) {
+        k_gather_roots<<<(unsigned)std::min<int64_t>((r.n_over + 255) / 256, 1024), 256, 0, s>>>(
+            r.roots, vals2.p, r.n_over, r.over_roots);
+        GSM_LAUNCH("k_gather_roots");
+        ++launches;
+        pos = r.n_over;
+    }
+    for (int b = kNB - 2; b >= 0; --b) {
         const int64_t nb = (int64_t)hb[b];
         if (nb == 0) continue;
         a.idx = vals2.p + pos;
@@ -592,17 +622,15 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
         a.next = sched.p + b;
         a.slab = nullptr;
         pos += nb;
-        a.dmax = b == kNB - 1 ? hmax : std::min(E.e[b], hmax);
+        a.dmax = std::min(E.e[b], hmax);
         ++launches;
         if (b == 0) {
             const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nb + 7) / 8, (int64_t)sms * 8));
             k_clique_warp<K><<<(unsigned)grid, 256, 0, s>>>(a);
             GSM_LAUNCH("k_clique_warp");
-        } else if (b == kNB - 1) {
+        } else if (b == kNB - 2) {
             const int64_t blocks = std::min<int64_t>(nb, sms);
             const CtaLay L = cta_lay(K, a.dmax, true, a.use_hash != 0);
-            if (cta_smem(K, a.dmax, true) > kSmemLim)
-                fail(GSM_ERR_OUT_OF_MEMORY, "clique path: |N+(u)| too large for the per-CTA hash/Bloom tables");
             slab.ensure((size_t)blocks * L.slab_ints, s);
             a.slab = slab.p;
             launch_cta<K, true, 1024>(a, blocks, s);
@@ -627,7 +655,8 @@ static int64_t run_clique_k(const CliqueRun& r, cudaStream_t s) {
     return launches;
 }
 
-int64_t run_clique(const CliqueRun& r, cudaStream_t s) {
+int64_t run_clique(CliqueRun& r, cudaStream_t s) {
+    r.n_over = 0;
     if (r.R <= 0) return 0;
     return r.k == 3 ? run_clique_k<3>(r, s) : run_clique_k<4>(r, s);
 }

@@ -125,8 +125,10 @@ struct CliqueRun {
     const int32_t* up;
     unsigned long long* count;
     unsigned long long* stats;  // 5: [list entries read, global probes, bitmap words, cliques, sum |N+(u)|]
+    int32_t* over_roots;    // out (capacity R): roots with |N+(u)| beyond the per-CTA tables,
+    int64_t n_over;         // left to the breadth-first path (set by run_clique)
 };
-int64_t run_clique(const CliqueRun& r, cudaStream_t s);  // returns kernel launches
+int64_t run_clique(CliqueRun& r, cudaStream_t s);  // returns kernel launches
 int clique_dsmem(int K);
 
 // Finalize ("Return ... subgraph enumeration M").

@@ -283,11 +283,16 @@ void Matcher::run() {
         cr.cols = g_.cols;
         cr.up = g_.up;
         cr.count = final_count_.p;
-        cr.stats = stats_.p + 5 * kMaxK;
+        cr.stats = stats_.p;  // slot 0 (the frontier levels use slots 1..k-1, the tail slot kMaxK)
+        DevBuf<int32_t> over;
+        over.ensure(R0, s_);
+        cr.over_roots = over.p;
         int64_t launches = 0;
         rec_.run(GSM_K_CLIQUE, 1, [&] { launches = run_clique(cr, s_); });
         res_->kernel_launches += launches > 0 ? launches - 1 : 0;
         res_->num_chunks++;
+        // roots whose N+(u) exceeds the per-CTA tables: the breadth-first path (same counter)
+        if (cr.n_over > 0) process(1, over.p, cr.n_over);
         found = read_scalar(final_count_.p, s_);
     } else if (R0 > 0) {
         process(1, lv_[1]->rows.p, R0);
@@ -315,11 +320,12 @@ void Matcher::run() {
         if (clique_) {
             // per root: id + offset pair + up (28 B); per S(u) entry: the entry and its own
             // offset pair + up (4 + 20 B); list entries streamed and binary-search probes (4 B)
-            const unsigned long long* st = hs.data() + 5 * kMaxK;
+            const unsigned long long* st = hs.data();
             res_->prof[GSM_K_CLIQUE].alg_bytes +=
                 28.0 * (double)R0 + 24.0 * (double)st[4] + 4.0 * (double)st[0] + 4.0 * (double)st[1];
             res_->level_work[k_ - 1] += st[0];
-        } else if (tail_) {
+        }
+        if (tail_) {
             const unsigned long long* st = hs.data() + 5 * kMaxK;
             const int w = k_ - 2;
             const LevelPlan& L = lplan_[w];

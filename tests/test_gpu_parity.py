@@ -151,16 +151,17 @@ def dense_gnp():
     return g, oracle.count_triangles(g), oracle.count_k4(g)
 
 
-@pytest.mark.parametrize("variant", ["default", "warp0", "dsmem64", "search", "stream", "nohash", "off"])
+@pytest.mark.parametrize("variant", ["default", "warp0", "dsmem64", "search", "stream", "nohash", "handback", "off"])
 def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
     """K3/K4 COUNT through the per-root local-bitmap kernels (gsm_clique.cu) in every
     bucket (warp per root; CTA with shared memory; CTA with a global slab via a tiny
     GSM_CLIQUE_DSMEM) and both row-construction strategies, against the oracle (DFS on an
     R-MAT graph, independent clique counters on a dense G(n, p)).  "off" = the fused-tail
-    path (GSM_CLIQUE=0) on the same inputs."""
+    path (GSM_CLIQUE=0) on the same inputs; "handback" = roots beyond GSM_CLIQUE_DMAX handed
+    back to the breadth-first path inside the same call."""
     env = {"warp0": {"GSM_CLIQUE_WARP": "0"}, "dsmem64": {"GSM_CLIQUE_DSMEM": "64"},
            "search": {"GSM_CLIQUE_STREAM": "0"}, "stream": {"GSM_CLIQUE_STREAM": "1000000000"},
-           "nohash": {"GSM_CLIQUE_HASH": "0"},
+           "nohash": {"GSM_CLIQUE_HASH": "0"}, "handback": {"GSM_CLIQUE_DMAX": "64"},
            "off": {"GSM_CLIQUE": "0"}}.get(variant, {})
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -181,7 +182,10 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
     try:
         assert run(G, gi.query("K3"), "count", flags=gsm.GSM_FLAG_UNIQUE)[0] == T, variant
         assert run(G, gi.query("K4"), "count", flags=gsm.GSM_FLAG_UNIQUE)[0] == K4, variant
-        assert run(G, gi.query("K4"), "count")[0] == 24 * K4, variant
+        c4, _, r4 = run(G, gi.query("K4"), "count")
+        assert c4 == 24 * K4, variant
+        if variant == "handback":  # roots with |N+(u)| > 64 went to the breadth-first path
+            assert r4.prof["tail"]["launches"] + r4.prof["expand"]["launches"] > 0, r4.prof
     finally:
         G.free()
 

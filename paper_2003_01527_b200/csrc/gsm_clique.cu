@@ -28,6 +28,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "gsm_kernels.h"
@@ -73,11 +74,7 @@ __device__ __forceinline__ unsigned ck_h0(int32_t v, unsigned P, unsigned seed) 
 }
 
 __device__ __forceinline__ unsigned ck_h1(int32_t v, unsigned P, unsigned seed) {
-    unsigned x = (unsigned)v ^ (0x5BD1E995u + seed);
-    x *= 0x85EBCA6Bu;
-    x ^= x >> 13;
-    x *= 0xC2B2AE35u;
-    return __umulhi(x, P);
+    return __umulhi(((unsigned)v + seed) * 0x85EBCA6Bu, P);
 }
 
 // local index of v in S(u), or -1
@@ -143,6 +140,7 @@ struct CliqueArgs {
     unsigned long long* next;   // dynamic root scheduler
     unsigned long long* count;  // unique cliques (atomic)
     unsigned long long* stats;  // [list entries read, global probes, bitmap words, cliques, sum |S(u)|]
+    unsigned long long* cyc;    // optional (GSM_TRACE=2): warp-cycles [setup, stream rows, search rows, level 3]
 };
 
 // ---------------------------------------------------------------------------- d <= 32
@@ -184,7 +182,20 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
                 }
                 bits = __reduce_or_sync(kFull, bits);
             } else {
-                const bool f = lane > i && lane < d && search_list(cols, ls, le, sv, probes);
+                // slice of N+(S[i]) by 32 splitters (see k_clique_cta), then binary search
+                const int64_t len = le - ls;
+                const int64_t bl = ls + ((int64_t)lane * len) / 32;
+                const int32_t spl = bl < le ? cols[bl] : INT32_MAX;
+                int lo = 0, hi = 32;
+#pragma unroll
+                for (int st = 0; st < 5; ++st) {
+                    const int mid = (lo + hi) >> 1;
+                    const int32_t x = __shfl_sync(kFull, spl, mid);
+                    if (x <= sv) lo = mid; else hi = mid;
+                }
+                const bool f = lane > i && lane < d &&
+                               search_list(cols, ls + ((int64_t)lo * len) / 32, ls + ((int64_t)(lo + 1) * len) / 32, sv,
+                                           probes);
                 bits = __ballot_sync(kFull, f);
                 items += (lane > i && lane < d);
             }
@@ -282,7 +293,10 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     unsigned* A = reinterpret_cast<unsigned*>(ws + L.A);
     unsigned long long cnt = 0, items = 0, words = 0, sent = 0;
     unsigned probes = 0;
+    unsigned long long cy[4] = {0, 0, 0, 0};
+    long long tc = 0;
     for (;;) {
+        if (a.cyc) tc = clock64();
         __syncthreads();
         if (threadIdx.x == 0) {
             sRoot = atomicAdd(a.next, 1ull);
@@ -344,6 +358,11 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         }
         __syncthreads();
         const int32_t smax = S[d - 1];
+        if (a.cyc) {
+            const long long t1 = clock64();
+            cy[0] += t1 - tc;
+            tc = t1;
+        }
         // ---- rows A[i] (level 1 -> 2 connection tests), warps take rows dynamically
         for (;;) {
             int i = 0;
@@ -372,7 +391,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int32_t v0 = x < le ? cols[x] : INT32_MAX;
                     const int32_t v1 = x + 32 < le ? cols[x + 32] : INT32_MAX;
                     if (!__any_sync(kFull, v0 <= smax)) break;
-                    items += (v0 <= smax) + (v1 <= smax);
+                    if (lane == 0) items += min((int64_t)64, le - x0);
                     const int j0 = ck_find(T, P, seed, v0);
                     const int j1 = ck_find(T, P, seed, v1);
                     if (K == 4) {
@@ -384,18 +403,43 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                         cnt += (j0 >= 0) + (j1 >= 0);
                     }
                 }
+                if (a.cyc) {
+                    const long long t1 = clock64();
+                    cy[1] += t1 - tc;
+                    tc = t1;
+                }
             } else {
+                // 32 splitters of N+(S[i]) in one coalesced load (lane l: the first entry of
+                // slice l); each key then picks its slice by a 5-step shuffle search and binary-
+                // searches only that slice in global memory (5 fewer dependent global probes)
+                const int64_t bl = ls + ((int64_t)lane * len) / 32;
+                const int32_t spl = bl < le ? cols[bl] : INT32_MAX;
                 for (int w = w0; w < W; ++w) {
                     const int j = (w << 5) + lane;
                     const bool live = j > i && j < d;
                     items += live;
-                    const bool f = live && search_list(cols, ls, le, S[j], probes);
+                    const int32_t key = live ? S[j] : INT32_MAX;
+                    int lo = 0, hi = 32;  // last slice whose first entry <= key
+#pragma unroll
+                    for (int st = 0; st < 5; ++st) {
+                        const int mid = (lo + hi) >> 1;
+                        const int32_t sv = __shfl_sync(kFull, spl, mid);
+                        if (sv <= key) lo = mid; else hi = mid;
+                    }
+                    const int64_t sb = ls + ((int64_t)lo * len) / 32;
+                    const int64_t se = ls + ((int64_t)(lo + 1) * len) / 32;
+                    const bool f = live && search_list(cols, sb, se, key, probes);
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
                         if (lane == 0) Ai[w] = bits;
                     } else {
                         cnt += f;
                     }
+                }
+                if (a.cyc) {
+                    const long long t1 = clock64();
+                    cy[2] += t1 - tc;
+                    tc = t1;
                 }
             }
         }
@@ -450,7 +494,10 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             }
             if (nJ > 0) flush(nJ);
         }
+        if (a.cyc) cy[3] += clock64() - tc;
     }
+    if (a.cyc && lane == 0)
+        for (int q = 0; q < 4; ++q) atomicAdd(&a.cyc[q], cy[q]);
     unsigned long long pr = probes;
     for (int o = 16; o; o >>= 1) {
         cnt += __shfl_xor_sync(kFull, cnt, o);
@@ -602,6 +649,14 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     a.stream_max = stream_max();
     a.use_hash = use_hash();
     a.dbg = getenv("GSM_CLIQUE_DBG") ? atoi(getenv("GSM_CLIQUE_DBG")) : 0;
+    DevBuf<unsigned long long> cyc;
+    a.cyc = nullptr;
+    const char* trace = getenv("GSM_TRACE");
+    if (trace && trace[0] == '2') {
+        cyc.ensure(4, s);
+        GSM_CUDA(cudaMemsetAsync(cyc.p, 0, 4 * sizeof(unsigned long long), s));
+        a.cyc = cyc.p;
+    }
     a.slab = nullptr;
     a.count = r.count;
     a.stats = r.stats;
@@ -651,6 +706,15 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
             else if (best == 512) launch_cta<K, false, 512>(a, nb, s);
             else launch_cta<K, false, 1024>(a, nb, s);
         }
+    }
+    if (a.cyc) {
+        unsigned long long hc[4];
+        GSM_CUDA(cudaMemcpyAsync(hc, a.cyc, sizeof(hc), cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        const double t = (double)(hc[0] + hc[1] + hc[2] + hc[3]) + 1e-9;
+        std::fprintf(stderr, "[gsm clique K%d] k_clique_cta warp-cycles: setup %.1f%%  stream rows %.1f%%  search rows %.1f%%"
+                     "  level 3 %.1f%%  (total %.3g)\n", K, 100 * hc[0] / t, 100 * hc[1] / t, 100 * hc[2] / t,
+                     100 * hc[3] / t, t);
     }
     return launches;
 }

@@ -1367,6 +1367,117 @@ int tail_block_cap() {  // per-CTA buffer for big rows (GSM_TAIL_BLOCK_CAP)
     return cap;
 }
 
+// ============================================================================
+// Pair tail (COUNT mode): the last two positions p, q are not adjacent in Q and carry
+// no ID condition between them, so given a row r of the first k-2 positions their
+// candidate sets (Alg. 1 line 12: label, degree, connections with the
+// mapped positions, injectivity) are independent and
+//     #{(x, y) : x ∈ Cp(r), y ∈ Cq(r), x != y} = |Cp| |Cq| - |Cp ∩ Cq|.
+// One warp per row: lanes stride the pivot segment of p (and then of q), each candidate
+// is verified against the other backward lists by binary search; |Cp ∩ Cq| re-checks
+// the survivors of p against q's constraints (skipped when the labels differ).
+// ============================================================================
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_pair(PairArgs a, LevelPlan Lp, LevelPlan Lq) {
+    const int lane = threadIdx.x & 31;
+    const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
+    const int W = Lp.width;
+    unsigned long long total = 0, items = 0;
+    unsigned probes = 0;
+    constexpr int64_t kChunk = 4;
+    int64_t cbase = 0, cend = 0;
+    for (;;) {
+        if (cbase >= cend) {
+            unsigned long long b = 0;
+            if (lane == 0) b = atomicAdd(a.next, (unsigned long long)kChunk);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if ((int64_t)b >= a.R) break;
+            cbase = (int64_t)b;
+            cend = min(cbase + kChunk, a.R);
+        }
+        const int64_t r = cbase++;
+        const int32_t* row = a.F + r * W;
+        unsigned long long cp = 0, cq = 0, cb = 0;
+        {   // candidates of p
+            const int64_t len = a.plen[r], beg = a.pbeg[r];
+            const int piv = a.ppiv[r];
+            for (int64_t x = lane; x < len; x += 32) {
+                const int32_t v = a.colsp[beg + x] & Lp.idmask;
+                ++items;
+                bool ok = true;
+                if (Lp.check_mask) ok = (cmask[v] >> Lp.qv) & 1u;
+                for (int t = 0; t < Lp.ninj && ok; ++t) ok = v != row[Lp.inj[t]];
+                for (int t = 0; t < Lp.nb && ok; ++t)
+                    if (t != piv)
+                        ok = in_sorted(a.colsp + a.pcbeg[r * Lp.nb + t], a.pclen[r * Lp.nb + t], Lp.key_base | v, probes);
+                cp += ok;
+                if (ok && a.need_both) {  // also a candidate of q?
+                    bool o2 = true;
+                    if (Lq.check_mask) o2 = (cmask[v] >> Lq.qv) & 1u;
+                    for (int t = 0; t < Lq.ninj && o2; ++t) o2 = v != row[Lq.inj[t]];
+                    for (int t = 0; t < Lq.nb && o2; ++t)
+                        o2 = in_sorted(a.colsq + a.qcbeg[r * Lq.nb + t], a.qclen[r * Lq.nb + t], Lq.key_base | v, probes);
+                    cb += o2;
+                }
+            }
+        }
+        {   // candidates of q
+            const int64_t len = a.qlen[r], beg = a.qbeg[r];
+            const int piv = a.qpiv[r];
+            for (int64_t x = lane; x < len; x += 32) {
+                const int32_t v = a.colsq[beg + x] & Lq.idmask;
+                ++items;
+                bool ok = true;
+                if (Lq.check_mask) ok = (cmask[v] >> Lq.qv) & 1u;
+                for (int t = 0; t < Lq.ninj && ok; ++t) ok = v != row[Lq.inj[t]];
+                for (int t = 0; t < Lq.nb && ok; ++t)
+                    if (t != piv)
+                        ok = in_sorted(a.colsq + a.qcbeg[r * Lq.nb + t], a.qclen[r * Lq.nb + t], Lq.key_base | v, probes);
+                cq += ok;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            cp += __shfl_xor_sync(0xffffffffu, cp, o);
+            cq += __shfl_xor_sync(0xffffffffu, cq, o);
+            cb += __shfl_xor_sync(0xffffffffu, cb, o);
+        }
+        total += cp * cq - cb;  // identical on every lane
+    }
+    unsigned long long pr = probes;
+    for (int o = 16; o; o >>= 1) {
+        items += __shfl_xor_sync(0xffffffffu, items, o);
+        pr += __shfl_xor_sync(0xffffffffu, pr, o);
+    }
+    if (lane == 0) {
+        if (total) {
+            atomicAdd(a.count, total);
+            atomicAdd(&a.stats[3], total);
+        }
+        if (items) atomicAdd(&a.stats[0], items);
+        if (pr) atomicAdd(&a.stats[2], pr);
+    }
+}
+
+template <typename MaskT>
+static void launch_pair_t(const PairArgs& a, const LevelPlan& Lp, const LevelPlan& Lq, cudaStream_t s) {
+    int dev = 0, sms = 148, per_sm = 1;
+    GSM_CUDA(cudaGetDevice(&dev));
+    GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pair<MaskT>, kThreads, 0));
+    const int64_t want = (a.R + kWarps - 1) / kWarps;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1)));
+    k_pair<MaskT><<<(unsigned)grid, kThreads, 0, s>>>(a, Lp, Lq);
+    GSM_LAUNCH("k_pair");
+}
+
+void launch_pair(const PairArgs& a, const LevelPlan& Lp, const LevelPlan& Lq, int mask_bytes, cudaStream_t s) {
+    switch (mask_bytes) {
+        case 1: launch_pair_t<uint8_t>(a, Lp, Lq, s); break;
+        case 2: launch_pair_t<uint16_t>(a, Lp, Lq, s); break;
+        default: launch_pair_t<uint32_t>(a, Lp, Lq, s); break;
+    }
+}
+
 __global__ void k_gather_len(const int64_t* __restrict__ rlen, const int64_t* __restrict__ idx, int64_t n,
                              int64_t* __restrict__ keys) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

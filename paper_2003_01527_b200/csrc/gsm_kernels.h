@@ -114,6 +114,27 @@ void launch_tail_block(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& 
 void launch_tail(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s);
 void launch_gather_rows(const int32_t* F, int W, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s);
 
+// Pair tail (COUNT mode): positions p = k-2 and q = k-1 not adjacent in Q and without an ID
+// condition between them: count(r) = |Cp(r)| |Cq(r)| - |Cp(r) ∩ Cq(r)| per row r of width k-2.
+struct PairArgs {
+    const int32_t* F;
+    int64_t R;
+    const int64_t *pbeg, *plen, *pcbeg;  // k_plan_rows of position p
+    const uint8_t* ppiv;
+    const int32_t* pclen;
+    const int64_t *qbeg, *qlen, *qcbeg;  // k_plan_rows of position q (same input rows)
+    const uint8_t* qpiv;
+    const int32_t* qclen;
+    const int32_t* colsp;   // plain or keyed lists of p's / q's label
+    const int32_t* colsq;
+    const void* cmask;
+    int32_t need_both;      // 0 when Cp and Cq are disjoint (different labels)
+    unsigned long long* count;
+    unsigned long long* next;   // dynamic row scheduler (zeroed)
+    unsigned long long* stats;  // [items, -, probes, -, -]
+};
+void launch_pair(const PairArgs& a, const LevelPlan& Lp, const LevelPlan& Lq, int mask_bytes, cudaStream_t s);
+
 // Clique queries K3/K4 in COUNT mode (gsm_clique.cu): per-root local bitmaps over
 // N+(u).  Adds the number of cliques (orbit representatives) to *count.
 struct CliqueRun {

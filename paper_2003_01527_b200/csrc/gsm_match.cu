@@ -102,6 +102,7 @@ class Matcher {
     void process(int w, const int32_t* F, int64_t R);
     void process_generic(int w, const int32_t* F, int64_t R);
     void process_tail(int w, const int32_t* F, int64_t R);
+    void process_pair(int w, const int32_t* F, int64_t R);
     bool tail_eligible(TailArgs* ta) const;
     bool clique_eligible() const;
     void append_output(const int32_t* rows, int64_t R);
@@ -134,6 +135,9 @@ class Matcher {
     TailArgs tail_args_;
     double tail_rows_ = 0;     // rows handled by the fused tail
     bool clique_ = false;      // K3/K4 COUNT: per-root local bitmaps (gsm_clique.cu)
+    bool pair_ = false;        // COUNT: last two positions independent (k_pair)
+    LevelPlan lq_;             // plan of position k-1 over rows of width k-2 (pair tail)
+    double pair_rows_ = 0;
 };
 
 void Matcher::run() {
@@ -188,6 +192,11 @@ void Matcher::run() {
     }
     // ---- query order with the exact |C(u)|
     compute_order(&plan_, cand, opts_.root_subset ? 0 : -1);
+    {   // COUNT mode: order the two last positions as an independent pair when Q allows it
+        const char* env = getenv("GSM_PAIR_TAIL");
+        if (count_mode_ && !opts_.root_subset && k_ >= 3 && !(env && env[0] == '0'))
+            pair_ = compute_order_pair_tail(&plan_, cand);
+    }
     for (int i = 0; i < k_; ++i) res_->order[i] = plan_.order[i];
     res_->num_levels = k_;
     res_->width = k_;
@@ -212,6 +221,15 @@ void Matcher::run() {
 
     tail_ = tail_eligible(&tail_args_);
     clique_ = clique_eligible();
+    if (pair_) {
+        tail_ = false;
+        lq_ = lplan_[k_ - 1];
+        lq_.width = k_ - 2;  // rows of the first k-2 positions; q never refers to p = k-2
+        int n = 0;
+        for (int t = 0; t < lq_.ninj; ++t)
+            if (lq_.inj[t] != k_ - 2) lq_.inj[n++] = lq_.inj[t];
+        lq_.ninj = n;
+    }
 
     // ---- roots = C(π[0]) (level-0 frontier)
     int64_t R0 = 0;
@@ -325,6 +343,13 @@ void Matcher::run() {
                 28.0 * (double)R0 + 24.0 * (double)st[4] + 4.0 * (double)st[0] + 4.0 * (double)st[1];
             res_->level_work[k_ - 1] += st[0];
         }
+        if (pair_) {  // staged row + both plans' segments; candidates and probes
+            const unsigned long long* st = hs.data() + 5 * kMaxK;
+            const int w = k_ - 2;
+            res_->prof[GSM_K_TAIL].alg_bytes += pair_rows_ * (4.0 * w + 2 * 17.0 + 12.0 * (lplan_[w].nb + lq_.nb)) +
+                                                4.0 * st[0] + 4.0 * st[2];
+            res_->level_work[k_ - 1] += st[0];
+        }
         if (tail_) {
             const unsigned long long* st = hs.data() + 5 * kMaxK;
             const int w = k_ - 2;
@@ -350,7 +375,8 @@ void Matcher::run() {
 
 void Matcher::process(int w, const int32_t* F, int64_t R) {
     if (R <= 0) return;
-    if (tail_ && w == k_ - 2) process_tail(w, F, R);
+    if (pair_ && w == k_ - 2) process_pair(w, F, R);
+    else if (tail_ && w == k_ - 2) process_tail(w, F, R);
     else process_generic(w, F, R);
 }
 
@@ -476,6 +502,56 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
         GSM_CUDA(cudaMemcpyAsync(rows.p, ovf_rows_.p, sizeof(int32_t) * nov * w, cudaMemcpyDeviceToDevice, s_));
         process_generic(w, rows.p, nov);
     }
+}
+
+// Pair tail (COUNT): per row of width k-2, |Cp| |Cq| - |Cp ∩ Cq| (k_pair)
+void Matcher::process_pair(int w, const int32_t* F, int64_t R) {
+    LevelBufs& B = *lv_[w];
+    const LevelPlan& Lp = lplan_[w];
+    B.rbeg.ensure(R, s_);
+    B.rlen.ensure(R, s_);
+    B.rpiv.ensure(R, s_);
+    B.cbeg.ensure((size_t)R * Lp.nb, s_);
+    B.clen.ensure((size_t)R * Lp.nb, s_);
+    DevBuf<int64_t> qbeg, qlen, qcbeg;
+    DevBuf<uint8_t> qpiv;
+    DevBuf<int32_t> qclen;
+    qbeg.ensure(R, s_);
+    qlen.ensure(R, s_);
+    qpiv.ensure(R, s_);
+    qcbeg.ensure((size_t)R * lq_.nb, s_);
+    qclen.ensure((size_t)R * lq_.nb, s_);
+    rec_.run(GSM_K_PLAN, 2, [&] {
+        launch_plan_rows(g_, F, R, Lp, B.rbeg.p, B.rlen.p, B.rpiv.p, B.cbeg.p, B.clen.p, s_);
+        launch_plan_rows(g_, F, R, lq_, qbeg.p, qlen.p, qpiv.p, qcbeg.p, qclen.p, s_);
+    });
+    res_->prof[GSM_K_PLAN].alg_bytes += (double)R * (2 * 4.0 * w + 28.0 * (Lp.nb + lq_.nb) + 2 * 17.0);
+    PairArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.F = F;
+    a.R = R;
+    a.pbeg = B.rbeg.p;
+    a.plen = B.rlen.p;
+    a.ppiv = B.rpiv.p;
+    a.pcbeg = B.cbeg.p;
+    a.pclen = B.clen.p;
+    a.qbeg = qbeg.p;
+    a.qlen = qlen.p;
+    a.qpiv = qpiv.p;
+    a.qcbeg = qcbeg.p;
+    a.qclen = qclen.p;
+    a.colsp = Lp.keyed ? g_.lkeys : g_.cols;
+    a.colsq = lq_.keyed ? g_.lkeys : g_.cols;
+    a.cmask = cmask_.p;
+    a.need_both = !(plan_.use_labels && plan_.qlabel[Lp.qv] != plan_.qlabel[lq_.qv]);
+    a.count = final_count_.p;
+    ws_.sched.ensure(1, s_);
+    GSM_CUDA(cudaMemsetAsync(ws_.sched.p, 0, sizeof(unsigned long long), s_));
+    a.next = ws_.sched.p;
+    a.stats = stats_.p + 5 * kMaxK;
+    rec_.run(GSM_K_TAIL, 1, [&] { launch_pair(a, Lp, lq_, mask_bytes_, s_); });
+    res_->num_chunks++;
+    pair_rows_ += (double)R;
 }
 
 void Matcher::process_generic(int w, const int32_t* F, int64_t R) {

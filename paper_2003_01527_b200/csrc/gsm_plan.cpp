@@ -158,14 +158,16 @@ void compute_symmetry(QueryPlan* plan, bool with_conditions, size_t list_cap) {
 }
 
 // ---------------------------------------------------------------- order
-void compute_order(QueryPlan* plan, const uint64_t* cand, int forced_first) {
-    QueryPlan& p = *plan;
+// Greedy order of the query vertices not in `excluded`, then `tail` (in order).
+static void order_greedy(QueryPlan& p, const uint64_t* cand, int forced_first, uint32_t excluded,
+                         const int* tail, int ntail) {
     uint32_t placed = 0;
-    for (int i = 0; i < p.k; ++i) {
+    const int nfree = p.k - ntail;
+    for (int i = 0; i < nfree; ++i) {
         int best = -1;
         int best_dm = -1;
         for (int u = 0; u < p.k; ++u) {
-            if ((placed >> u) & 1u) continue;
+            if (((placed | excluded) >> u) & 1u) continue;
             int dm = __builtin_popcount(p.adj[u] & placed);
             if (i > 0 && dm == 0) continue;  // keep the prefix connected
             if (best < 0) { best = u; best_dm = dm; continue; }
@@ -182,6 +184,10 @@ void compute_order(QueryPlan* plan, const uint64_t* cand, int forced_first) {
         p.pos[best] = i;
         placed |= 1u << best;
     }
+    for (int t = 0; t < ntail; ++t) {
+        p.order[nfree + t] = tail[t];
+        p.pos[tail[t]] = nfree + t;
+    }
     for (int i = 0; i < p.k; ++i) {
         int u = p.order[i];
         p.backward[i] = 0;
@@ -192,6 +198,47 @@ void compute_order(QueryPlan* plan, const uint64_t* cand, int forced_first) {
                 if (p.parent[i] < 0) p.parent[i] = j;  // earliest-ordered neighbour
             }
     }
+}
+
+void compute_order(QueryPlan* plan, const uint64_t* cand, int forced_first) {
+    order_greedy(*plan, cand, forced_first, 0u, nullptr, 0);
+}
+
+// vertices of `mask` connected in Q (restricted to mask)
+static bool connected_within(const QueryPlan& p, uint32_t mask) {
+    if (!mask) return false;
+    uint32_t seen = mask & (~mask + 1u), frontier = seen;
+    while (frontier) {
+        uint32_t next = 0;
+        for (int u = 0; u < p.k; ++u)
+            if ((frontier >> u) & 1u) next |= p.adj[u] & mask;
+        frontier = next & ~seen;
+        seen |= next;
+    }
+    return seen == mask;
+}
+
+bool compute_order_pair_tail(QueryPlan* plan, const uint64_t* cand) {
+    QueryPlan& p = *plan;
+    if (p.k < 3) return false;
+    const uint32_t all = p.k == 32 ? 0xffffffffu : ((1u << p.k) - 1u);
+    int ba = -1, bb = -1;
+    double bestv = -1;
+    for (int a = 0; a < p.k; ++a)
+        for (int b = a + 1; b < p.k; ++b) {
+            if (qadj(p, a, b)) continue;
+            bool cond = false;
+            for (auto& c : p.conds)
+                if ((c.first == a && c.second == b) || (c.first == b && c.second == a)) cond = true;
+            if (cond) continue;
+            if (!connected_within(p, all & ~((1u << a) | (1u << b)))) continue;
+            const double v = cand ? (double)cand[a] * (double)cand[b] : 1.0;
+            if (v > bestv) { bestv = v; ba = a; bb = b; }
+        }
+    if (ba < 0) return false;
+    const int tail[2] = {ba, bb};
+    order_greedy(p, cand, -1, (1u << ba) | (1u << bb), tail, 2);
+    return true;
 }
 
 LevelPlan make_level_plan(const QueryPlan& p, int i, bool count_only) {

@@ -190,6 +190,33 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
         G.free()
 
 
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_pair_tail(pair, monkeypatch):
+    """COUNT mode with the last two positions an independent pair (k_pair: |Cp||Cq| - |Cp∩Cq|)
+    against the oracle's count, labeled and unlabeled, with and without symmetry; "0" =
+    the pair ordering disabled (GSM_PAIR_TAIL=0) on the same inputs."""
+    monkeypatch.setenv("GSM_PAIR_TAIL", pair)
+    g = gi.rmat(9, 8, seed=31).with_labels(gi.uniform_labels(512, 3, 31))
+    G = load(g)
+    try:
+        qs = [gi.query("P3"), gi.query("P4"), gi.query("S3"), gi.query("house"), gi.query("tailed_triangle"),
+              gi.query("P4", [0, 1, 2, 0]), gi.query("P4", [0, 1, 1, 2]), gi.query("S3", [0, 1, 1, 2]),
+              gi.query("house", [0, 1, 2, 0, 1]), gi.query("house", [0, 0, 1, 1, 2]), gi.query("C4", [0, 1, 0, 2])]
+        qs += [gi.random_connected_query(k, e, seed, 3) for (k, e, seed) in [(4, 1, 1), (5, 1, 2), (5, 2, 3), (6, 2, 4)]]
+        used = 0
+        for q in qs:  # unlabeled queries ignore the data labels (SURVEY §8(b))
+            cnt, _ = oracle.match(g, q, count_only=True)
+            for flags in (0, gsm.GSM_FLAG_NO_SYMMETRY):
+                c, _, r = run(G, q, "count", flags=flags)
+                assert c == cnt, (pair, q.name, q.labels, flags, c, cnt)
+                a, b = r.order[-2], r.order[-1]
+                adj = any({a, b} == {x, y} for x, y in q.edges)
+                used += (not adj) and r.prof["tail"]["launches"] > 0
+        assert (used > 0) == (pair == "1"), used
+    finally:
+        G.free()
+
+
 def test_ne_refinement_is_sound():
     """NE filter + refinement rounds (Alg. 1 lines 7-8): results
     identical for R = 0..3; |C(u)| non-increasing in R and never below the number of
@@ -431,9 +458,9 @@ def test_device_pointer_load_and_profile():
     try:
         c, _, r = run(G, gi.query("K3"), flags=gsm.GSM_FLAG_PROFILE)
         assert c == 6 * oracle.count_triangles(g)
-        hot = r.prof["expand"]["launches"] + r.prof["tail"]["launches"]
-        assert hot >= 1 and r.prof["expand"]["ms"] + r.prof["tail"]["ms"] > 0
-        assert r.prof["expand"]["alg_bytes"] + r.prof["tail"]["alg_bytes"] > 0 and r.prof["filter"]["ms"] > 0
+        hot = [r.prof[k] for k in ("expand", "tail", "clique")]
+        assert sum(h["launches"] for h in hot) >= 1 and sum(h["ms"] for h in hot) > 0
+        assert sum(h["alg_bytes"] for h in hot) > 0 and r.prof["filter"]["ms"] > 0
         rt = run(G, gi.query("K3"), "enumerate")[1]
         re = gsm.gsm_match(G, 3, gi.query("K3").edges, mode=gsm.GSM_MODE_ENUMERATE)
         t = re.rows_torch()

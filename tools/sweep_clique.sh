@@ -1,4 +1,3 @@
-# clique-path timing experiments on the GPU box (R-MAT-24 K3+K4)
-timeout 600 python -m pytest tests/test_gpu_parity.py -k "clique" -x -q > gpurun_out/t_clique10.log 2>&1; echo rc=$? >> gpurun_out/t_clique10.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -k "clique" -x -q > gpurun_out/t_clique11.log 2>&1; echo rc=$? >> gpurun_out/t_clique11.log
 GSM_TRACE=2 python tools/probe_overhead.py rmat24 0 2>&1 | tail -3
-python tools/probe_overhead.py rmat24 0 2>&1 | tail -3
+python tools/probe_overhead.py rmat24 0 2>&1 | tail -2

@@ -1395,7 +1395,8 @@ __global__ void __launch_bounds__(kThreads) k_pair(PairArgs a, LevelPlan Lp, Lev
             cbase = (int64_t)b;
             cend = min(cbase + kChunk, a.R);
         }
-        const int64_t r = cbase++;
+        const int64_t ri = cbase++;
+        const int64_t r = a.rows_idx ? a.rows_idx[ri] : ri;
         const int32_t* row = a.F + r * W;
         unsigned long long cp = 0, cq = 0, cb = 0;
         {   // candidates of p
@@ -1455,6 +1456,89 @@ __global__ void __launch_bounds__(kThreads) k_pair(PairArgs a, LevelPlan Lp, Lev
         }
         if (items) atomicAdd(&a.stats[0], items);
         if (pr) atomicAdd(&a.stats[2], pr);
+    }
+}
+
+// one thread per row (short segments); rows above a.thread_max candidates go to the warp pass
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_pair_thread(PairArgs a, LevelPlan Lp, LevelPlan Lq) {
+    const MaskT* __restrict__ cmask = static_cast<const MaskT*>(a.cmask);
+    const int W = Lp.width;
+    unsigned long long total = 0, items = 0;
+    unsigned probes = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.R; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t plen = a.plen[r], qlen = a.qlen[r];
+        if (plen == 0 || qlen == 0) continue;  // no candidate for p or q: nothing to count
+        if (plen + qlen > a.thread_max) {
+            a.overflow[atomicAdd(a.noverflow, 1ull)] = r;
+            continue;
+        }
+        const int32_t* row = a.F + r * W;
+        unsigned long long cp = 0, cq = 0, cb = 0;
+        const int64_t pb = a.pbeg[r], qb = a.qbeg[r];
+        const int ppv = a.ppiv[r], qpv = a.qpiv[r];
+        for (int64_t x = 0; x < plen; ++x) {
+            const int32_t v = a.colsp[pb + x] & Lp.idmask;
+            bool ok = true;
+            if (Lp.check_mask) ok = (cmask[v] >> Lp.qv) & 1u;
+            for (int t = 0; t < Lp.ninj && ok; ++t) ok = v != row[Lp.inj[t]];
+            for (int t = 0; t < Lp.nb && ok; ++t)
+                if (t != ppv)
+                    ok = in_sorted(a.colsp + a.pcbeg[r * Lp.nb + t], a.pclen[r * Lp.nb + t], Lp.key_base | v, probes);
+            cp += ok;
+            if (ok && a.need_both) {
+                bool o2 = true;
+                if (Lq.check_mask) o2 = (cmask[v] >> Lq.qv) & 1u;
+                for (int t = 0; t < Lq.ninj && o2; ++t) o2 = v != row[Lq.inj[t]];
+                for (int t = 0; t < Lq.nb && o2; ++t)
+                    o2 = in_sorted(a.colsq + a.qcbeg[r * Lq.nb + t], a.qclen[r * Lq.nb + t], Lq.key_base | v, probes);
+                cb += o2;
+            }
+        }
+        if (cp == 0) {
+            items += plen;
+            continue;
+        }
+        for (int64_t x = 0; x < qlen; ++x) {
+            const int32_t v = a.colsq[qb + x] & Lq.idmask;
+            bool ok = true;
+            if (Lq.check_mask) ok = (cmask[v] >> Lq.qv) & 1u;
+            for (int t = 0; t < Lq.ninj && ok; ++t) ok = v != row[Lq.inj[t]];
+            for (int t = 0; t < Lq.nb && ok; ++t)
+                if (t != qpv)
+                    ok = in_sorted(a.colsq + a.qcbeg[r * Lq.nb + t], a.qclen[r * Lq.nb + t], Lq.key_base | v, probes);
+            cq += ok;
+        }
+        items += plen + qlen;
+        total += cp * cq - cb;
+    }
+    unsigned long long pr = probes;
+    for (int o = 16; o; o >>= 1) {
+        total += __shfl_xor_sync(0xffffffffu, total, o);
+        items += __shfl_xor_sync(0xffffffffu, items, o);
+        pr += __shfl_xor_sync(0xffffffffu, pr, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (total) {
+            atomicAdd(a.count, total);
+            atomicAdd(&a.stats[3], total);
+        }
+        if (items) atomicAdd(&a.stats[0], items);
+        if (pr) atomicAdd(&a.stats[2], pr);
+    }
+}
+
+template <typename MaskT>
+static void launch_pair_thread_t(const PairArgs& a, const LevelPlan& Lp, const LevelPlan& Lq, cudaStream_t s) {
+    k_pair_thread<MaskT><<<grid_for(a.R), kThreads, 0, s>>>(a, Lp, Lq);
+    GSM_LAUNCH("k_pair_thread");
+}
+
+void launch_pair_thread(const PairArgs& a, const LevelPlan& Lp, const LevelPlan& Lq, int mask_bytes, cudaStream_t s) {
+    switch (mask_bytes) {
+        case 1: launch_pair_thread_t<uint8_t>(a, Lp, Lq, s); break;
+        case 2: launch_pair_thread_t<uint16_t>(a, Lp, Lq, s); break;
+        default: launch_pair_thread_t<uint32_t>(a, Lp, Lq, s); break;
     }
 }
 

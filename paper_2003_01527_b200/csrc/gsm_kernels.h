@@ -132,7 +132,14 @@ struct PairArgs {
     unsigned long long* count;
     unsigned long long* next;   // dynamic row scheduler (zeroed)
     unsigned long long* stats;  // [items, -, probes, -, -]
+    const int64_t* rows_idx;    // warp pass: the rows to process (NULL = 0..R-1)
+    int64_t* overflow;          // thread pass: rows whose two segments exceed `thread_max`
+    unsigned long long* noverflow;
+    int32_t thread_max;
 };
+// Thread pass: one thread per row for rows with short segments (labeled queries: most);
+// longer rows are appended to a.overflow for the warp pass (launch_pair).
+void launch_pair_thread(const PairArgs& a, const LevelPlan& Lp, const LevelPlan& Lq, int mask_bytes, cudaStream_t s);
 void launch_pair(const PairArgs& a, const LevelPlan& Lp, const LevelPlan& Lq, int mask_bytes, cudaStream_t s);
 
 // Clique queries K3/K4 in COUNT mode (gsm_clique.cu): per-root local bitmaps over

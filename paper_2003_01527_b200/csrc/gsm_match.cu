@@ -549,7 +549,22 @@ void Matcher::process_pair(int w, const int32_t* F, int64_t R) {
     GSM_CUDA(cudaMemsetAsync(ws_.sched.p, 0, sizeof(unsigned long long), s_));
     a.next = ws_.sched.p;
     a.stats = stats_.p + 5 * kMaxK;
-    rec_.run(GSM_K_TAIL, 1, [&] { launch_pair(a, Lp, lq_, mask_bytes_, s_); });
+    // thread per row for short segments, the rest (appended to an overflow list) warp per row
+    const int thread_max = getenv("GSM_PAIR_THREAD_MAX") ? atoi(getenv("GSM_PAIR_THREAD_MAX")) : 16;  // measured: 16 ~ 64 > 0 > 256
+    ovf_idx_.ensure(R, s_);
+    ovf_n_.ensure(1, s_);
+    GSM_CUDA(cudaMemsetAsync(ovf_n_.p, 0, sizeof(unsigned long long), s_));
+    a.overflow = ovf_idx_.p;
+    a.noverflow = ovf_n_.p;
+    a.thread_max = thread_max;
+    rec_.run(GSM_K_TAIL, 1, [&] { launch_pair_thread(a, Lp, lq_, mask_bytes_, s_); });
+    const int64_t nov = (int64_t)read_scalar(ovf_n_.p, s_);
+    if (nov > 0) {
+        PairArgs b = a;
+        b.R = nov;
+        b.rows_idx = ovf_idx_.p;
+        rec_.run(GSM_K_TAIL, 1, [&] { launch_pair(b, Lp, lq_, mask_bytes_, s_); });
+    }
     res_->num_chunks++;
     pair_rows_ += (double)R;
 }

@@ -190,12 +190,15 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
         G.free()
 
 
-@pytest.mark.parametrize("pair", ["1", "0"])
+@pytest.mark.parametrize("pair", ["1", "warp", "0"])
 def test_pair_tail(pair, monkeypatch):
     """COUNT mode with the last two positions an independent pair (k_pair: |Cp||Cq| - |Cp∩Cq|)
     against the oracle's count, labeled and unlabeled, with and without symmetry; "0" =
-    the pair ordering disabled (GSM_PAIR_TAIL=0) on the same inputs."""
-    monkeypatch.setenv("GSM_PAIR_TAIL", pair)
+    the pair ordering disabled (GSM_PAIR_TAIL=0) on the same inputs; "warp" = every row through
+    the warp-per-row kernel (no thread-per-row pass)."""
+    monkeypatch.setenv("GSM_PAIR_TAIL", "0" if pair == "0" else "1")
+    if pair == "warp":
+        monkeypatch.setenv("GSM_PAIR_THREAD_MAX", "0")
     g = gi.rmat(9, 8, seed=31).with_labels(gi.uniform_labels(512, 3, 31))
     G = load(g)
     try:
@@ -212,7 +215,7 @@ def test_pair_tail(pair, monkeypatch):
                 a, b = r.order[-2], r.order[-1]
                 adj = any({a, b} == {x, y} for x, y in q.edges)
                 used += (not adj) and r.prof["tail"]["launches"] > 0
-        assert (used > 0) == (pair == "1"), used
+        assert (used > 0) == (pair != "0"), used
     finally:
         G.free()
 

@@ -10,6 +10,7 @@
 // N+(v) = {w in N(v) : v ≺ w} is the contiguous suffix of v's sorted list
 // starting at up[v].  Every id crossing the ABI is an original id.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <chrono>
@@ -131,6 +132,20 @@ __global__ void k_edge_keys(const int64_t* __restrict__ off, const int32_t* __re
     }
 }
 
+// warp per new vertex p: its old list mapped to new ids (unsorted), at the new offset
+__global__ void k_edge_cols(const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                            const int64_t* __restrict__ noff, const int32_t* __restrict__ new2old,
+                            const int32_t* __restrict__ old2new, int64_t n, int32_t* out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = warp; p < n; p += nwarps) {
+        const int32_t old = new2old[p];
+        const int64_t b = off[old], e = off[old + 1], dst = noff[p];
+        for (int64_t i = b + lane; i < e; i += 32) out[dst + (i - b)] = old2new[cols[i]];
+    }
+}
+
 __global__ void k_extract_cols(const uint64_t* __restrict__ ekeys, int64_t nnz, int32_t* cols) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
         cols[i] = (int32_t)(ekeys[i] & 0xffffffffu);
@@ -196,14 +211,12 @@ static void free_graph(gsm_graph* h) {
     DevGraph& g = h->g;
     cudaStreamSynchronize(h->stream);
     h->ws.reset();  // frees the cached match workspace (stream-ordered)
+    // graph arrays come from the device's stream-ordered pool (kept cached by its release
+    // threshold, so a load/free/load cycle does not re-map memory)
+    for (void* p : {(void*)g.off, (void*)g.cols, (void*)g.up, (void*)g.labels, (void*)g.lkeys, (void*)g.new2old,
+                    (void*)g.old2new})
+        if (p) cudaFreeAsync(p, h->stream);
     cudaStreamSynchronize(h->stream);
-    cudaFree(g.off);
-    cudaFree(g.cols);
-    cudaFree(g.up);
-    cudaFree(g.labels);
-    cudaFree(g.lkeys);
-    cudaFree(g.new2old);
-    cudaFree(g.old2new);
     if (h->own_stream) cudaStreamDestroy(h->stream);
     cudaSetDevice(cur);
     delete h;
@@ -291,11 +304,11 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
     DevGraph& g = h->g;
     g.n = n;
     g.nnz = nnz;
-    GSM_CUDA(cudaMalloc(&g.off, sizeof(int64_t) * (n + 1)));
-    GSM_CUDA(cudaMalloc(&g.cols, sizeof(int32_t) * (nnz ? nnz : 1)));
-    GSM_CUDA(cudaMalloc(&g.up, sizeof(int32_t) * n));
-    GSM_CUDA(cudaMalloc(&g.new2old, sizeof(int32_t) * n));
-    GSM_CUDA(cudaMalloc(&g.old2new, sizeof(int32_t) * n));
+    g.off = static_cast<int64_t*>(dev_alloc(sizeof(int64_t) * (n + 1), s));
+    g.cols = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * (nnz ? nnz : 1), s));
+    g.up = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
+    g.new2old = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
+    g.old2new = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
 
     // 1. rank by (degree, id)
     {
@@ -328,8 +341,9 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         stmp.ensure(sb, s);
         GSM_CUDA(cub::DeviceScan::InclusiveSum(stmp.p, sb, newdeg.p, g.off + 1, n, s));
     }
-    // 2. relabelled, re-sorted lists
-    if (nnz > 0) {
+    // 2. relabelled lists, each re-sorted (segmented sort of 32-bit ids: the rows are
+    //    already in their new order, only the ids inside a list move)
+    if (nnz > 0 && nnz > (int64_t)INT32_MAX) {  // beyond 32-bit segmented-sort sizes: (row, id) keys
         DevBuf<uint64_t> ekeys, esorted;
         ekeys.ensure(nnz, s);
         esorted.ensure(nnz, s);
@@ -343,11 +357,21 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         GSM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, ekeys.p, esorted.p, nnz, 0, end_bit, s));
         k_extract_cols<<<grid_for(nnz), 256, 0, s>>>(esorted.p, nnz, g.cols);
         GSM_LAUNCH("k_extract_cols");
+    } else if (nnz > 0) {
+        DevBuf<int32_t> ecols;
+        ecols.ensure(nnz, s);
+        k_edge_cols<<<grid_for(n * 32), 256, 0, s>>>(d_off, d_cols, g.off, g.new2old, g.old2new, n, ecols.p);
+        GSM_LAUNCH("k_edge_cols");
+        size_t tmp_bytes = 0;
+        GSM_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, ecols.p, g.cols, nnz, n, g.off, g.off + 1, s));
+        DevBuf<uint8_t> tmp;
+        tmp.ensure(tmp_bytes, s);
+        GSM_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.p, tmp_bytes, ecols.p, g.cols, nnz, n, g.off, g.off + 1, s));
     }
     k_up<<<grid_for(n), 256, 0, s>>>(g.off, g.cols, n, g.up);
     GSM_LAUNCH("k_up");
     if (labels) {
-        GSM_CUDA(cudaMalloc(&g.labels, sizeof(uint32_t) * n));
+        g.labels = static_cast<uint32_t*>(dev_alloc(sizeof(uint32_t) * n, s));
         k_permute_labels<<<grid_for(n), 256, 0, s>>>(d_lab, g.new2old, n, g.labels);
         GSM_LAUNCH("k_permute_labels");
         h->labeled = true;
@@ -366,7 +390,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         g.max_label = hmax;
         if (nnz > 0 && idbits + lbits <= 31) {
             g.idbits = idbits;
-            GSM_CUDA(cudaMalloc(&g.lkeys, sizeof(int32_t) * nnz));
+            g.lkeys = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * nnz, s));
             DevBuf<uint64_t> ekeys, esorted;
             ekeys.ensure(nnz, s);
             esorted.ensure(nnz, s);

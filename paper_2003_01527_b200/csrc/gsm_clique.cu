@@ -77,13 +77,18 @@ __device__ __forceinline__ unsigned ck_h1(int32_t v, unsigned P, unsigned seed) 
     return __umulhi(((unsigned)v + seed) * 0x85EBCA6Bu, P);
 }
 
-// local index of v in S(u), or -1
-__device__ __forceinline__ int ck_find(const unsigned long long* T, unsigned P, unsigned seed, int32_t v) {
-    const unsigned long long e0 = T[ck_h0(v, P, seed)];
-    const unsigned long long e1 = T[P + ck_h1(v, P, seed)];
-    const bool m0 = (int32_t)(e0 >> 32) == v;
-    const bool m1 = (int32_t)(e1 >> 32) == v;
-    return m0 ? (int)(unsigned)e0 : (m1 ? (int)(unsigned)e1 : -1);
+// Tables as two 32-bit arrays: keys Tk[2P] (-1 = empty) and local indices Tj[2P].  A lookup
+// reads two 32-bit keys (half the shared-memory wavefronts of 64-bit entries); the index is
+// read only on a hit.  Returns the local index of v in S(u), or -1.
+__device__ __forceinline__ int ck_find(const int32_t* Tk, const int32_t* Tj, unsigned P, unsigned seed, int32_t v) {
+    const unsigned s0 = ck_h0(v, P, seed), s1 = P + ck_h1(v, P, seed);
+    const bool m0 = Tk[s0] == v;
+    const bool m1 = Tk[s1] == v;
+    return (m0 | m1) ? Tj[m0 ? s0 : s1] : -1;
+}
+
+__device__ __forceinline__ bool ck_has(const int32_t* Tk, unsigned P, unsigned seed, int32_t v) {
+    return (Tk[ck_h0(v, P, seed)] == v) | (Tk[P + ck_h1(v, P, seed)] == v);
 }
 
 }  // namespace
@@ -284,7 +289,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     const int32_t* __restrict__ cols = a.cols;
     const CtaLay L = cta_lay(K, a.dmax, kGlobal, a.use_hash != 0);
     int32_t* ws = kGlobal ? a.slab + (int64_t)blockIdx.x * L.slab_ints : csm;
-    unsigned long long* T = reinterpret_cast<unsigned long long*>(csm + L.h);
+    int32_t* Tk = csm + L.h;  // cuckoo keys [2P], then local indices [2P] (Tj)
     __shared__ int sFail;
     int32_t* TB = csm + L.tb;  // TB[b] = first word of row block b, TB[W + 1 + b] = its row length
     int32_t* S = ws + L.s;
@@ -336,24 +341,33 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 use_ck = false;
                 break;
             }
-            for (int h = threadIdx.x; h < 2 * (int)P; h += NT) T[h] = ~0ull;
+            for (int h = threadIdx.x; h < 2 * (int)P; h += NT) Tk[h] = -1;
             if (threadIdx.x == 0) sFail = 0;
             __syncthreads();
             for (int j = threadIdx.x; j < d; j += NT) {
-                unsigned long long e = ((unsigned long long)(unsigned)cols[s0 + j] << 32) | (unsigned)j;
+                int32_t e = S[j];
                 int tbl = 0;
                 int it = 0;
                 for (; it < 64; ++it) {
-                    const int32_t key = (int32_t)(e >> 32);
-                    const unsigned slot = tbl ? P + ck_h1(key, P, seed) : ck_h0(key, P, seed);
-                    e = atomicExch(&T[slot], e);
-                    if (e == ~0ull) break;
+                    const unsigned slot = tbl ? P + ck_h1(e, P, seed) : ck_h0(e, P, seed);
+                    e = atomicExch(&Tk[slot], e);
+                    if (e == -1) break;
                     tbl ^= 1;
                 }
                 if (it == 64) sFail = 1;
             }
             __syncthreads();
-            if (!sFail) break;
+            if (!sFail) {
+                if (K == 4) {  // local indices next to the settled keys
+                    int32_t* Tj = Tk + 2 * P;
+                    for (int j = threadIdx.x; j < d; j += NT) {
+                        const int32_t v = S[j];
+                        const unsigned s0h = ck_h0(v, P, seed);
+                        Tj[Tk[s0h] == v ? s0h : P + ck_h1(v, P, seed)] = j;
+                    }
+                }
+                break;
+            }
             __syncthreads();
         }
         __syncthreads();
@@ -392,8 +406,8 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int32_t v1 = x + 32 < le ? cols[x + 32] : INT32_MAX;
                     if (!__any_sync(kFull, v0 <= smax)) break;
                     if (lane == 0) items += min((int64_t)64, le - x0);
-                    const int j0 = ck_find(T, P, seed, v0);
-                    const int j1 = ck_find(T, P, seed, v1);
+                    const int j0 = K == 4 ? ck_find(Tk, Tk + 2 * P, P, seed, v0) : (ck_has(Tk, P, seed, v0) ? 0 : -1);
+                    const int j1 = K == 4 ? ck_find(Tk, Tk + 2 * P, P, seed, v1) : (ck_has(Tk, P, seed, v1) ? 0 : -1);
                     if (K == 4) {
                         if (!(a.dbg & 2)) {
                             if (j0 >= 0) atomicOr(&Ai[j0 >> 5], 1u << (j0 & 31));

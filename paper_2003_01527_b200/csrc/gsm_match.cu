@@ -513,9 +513,14 @@ void Matcher::process_pair(int w, const int32_t* F, int64_t R) {
     B.rpiv.ensure(R, s_);
     B.cbeg.ensure((size_t)R * Lp.nb, s_);
     B.clen.ensure((size_t)R * Lp.nb, s_);
-    DevBuf<int64_t> qbeg, qlen, qcbeg;
-    DevBuf<uint8_t> qpiv;
-    DevBuf<int32_t> qclen;
+    // q's plan goes to the width-(k-1) level buffers: with the pair tail that level is never
+    // expanded, and the per-graph workspace keeps them across calls (no pool round trip)
+    LevelBufs& Q = *lv_[k_ - 1];
+    DevBuf<int64_t>& qbeg = Q.rbeg;
+    DevBuf<int64_t>& qlen = Q.rlen;
+    DevBuf<uint8_t>& qpiv = Q.rpiv;
+    DevBuf<int64_t>& qcbeg = Q.cbeg;
+    DevBuf<int32_t>& qclen = Q.clen;
     qbeg.ensure(R, s_);
     qlen.ensure(R, s_);
     qpiv.ensure(R, s_);

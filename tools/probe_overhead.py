@@ -9,7 +9,7 @@ from paper_2003_01527_b200 import gsm
 
 w = workloads.get(sys.argv[1] if len(sys.argv) > 1 else "rmat24")
 g = w.graph() if callable(getattr(w, "graph", None)) else w.graph
-G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, None, device=0)
+G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=0)
 s = torch.cuda.current_stream().cuda_stream
 for it in range(4):
     ev0 = torch.cuda.Event(enable_timing=True); ev1 = torch.cuda.Event(enable_timing=True)

@@ -32,6 +32,7 @@
 #include <cstdlib>
 
 #include "gsm_kernels.h"
+#include "gsm_workspace.h"
 
 namespace gsm {
 
@@ -620,9 +621,11 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     const int dglob = clique_dglob(K);
     const int e[kNB - 1] = {warp_max(), 128, 256, 512, K == 4 ? 960 : 1024, dsmem, std::max(dsmem, dglob)};
     for (int b = 0; b < kNB - 1; ++b) E.e[b] = std::min(e[b], dglob);
-    DevBuf<int32_t> keys, vals, keys2, vals2, slab;
-    DevBuf<unsigned long long> bucket, sched;
-    DevBuf<int> dmax;
+    Workspace& W_ = *r.ws;  // grow-only, kept with the graph (no pool round trips per call)
+    DevBuf<int32_t>&keys = W_.ck_keys, &vals = W_.ck_vals, &keys2 = W_.ck_keys2, &vals2 = W_.ck_vals2,
+                   &slab = W_.ck_slab;
+    DevBuf<unsigned long long>&bucket = W_.ck_bucket, &sched = W_.ck_sched;
+    DevBuf<int>& dmax = W_.ck_dmax;
     keys.ensure(R, s);
     vals.ensure(R, s);
     keys2.ensure(R, s);
@@ -650,7 +653,7 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     size_t tb = 0;
     GSM_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, keys.p, keys2.p, vals.p, vals2.p, (int)R, 0,
                                                        end_bit, s));
-    DevBuf<uint8_t> tmp;
+    DevBuf<uint8_t>& tmp = W_.ck_tmp;
     tmp.ensure(tb, s);
     GSM_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, keys.p, keys2.p, vals.p, vals2.p, (int)R, 0,
                                                        end_bit, s));

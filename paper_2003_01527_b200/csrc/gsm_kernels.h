@@ -155,6 +155,7 @@ struct CliqueRun {
     unsigned long long* stats;  // 5: [list entries read, global probes, bitmap words, cliques, sum |N+(u)|]
     int32_t* over_roots;    // out (capacity R): roots with |N+(u)| beyond the per-CTA tables,
     int64_t n_over;         // left to the breadth-first path (set by run_clique)
+    struct Workspace* ws;   // per-graph grow-only buffers (gsm_workspace.h)
 };
 int64_t run_clique(CliqueRun& r, cudaStream_t s);  // returns kernel launches
 int clique_dsmem(int K);

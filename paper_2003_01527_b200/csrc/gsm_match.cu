@@ -302,9 +302,10 @@ void Matcher::run() {
         cr.up = g_.up;
         cr.count = final_count_.p;
         cr.stats = stats_.p;  // slot 0 (the frontier levels use slots 1..k-1, the tail slot kMaxK)
-        DevBuf<int32_t> over;
+        DevBuf<int32_t>& over = ws_.ck_over;
         over.ensure(R0, s_);
         cr.over_roots = over.p;
+        cr.ws = &ws_;
         int64_t launches = 0;
         rec_.run(GSM_K_CLIQUE, 1, [&] { launches = run_clique(cr, s_); });
         res_->kernel_launches += launches > 0 ? launches - 1 : 0;

@@ -27,6 +27,11 @@ struct Workspace {
     DevBuf<unsigned long long> counts, final_count, stats, ovf_n, sched;
     DevBuf<int64_t> ovf_idx;
     DevBuf<int32_t> ovf_rows;
+    // clique path (gsm_clique.cu): root keys / order, sort temp, global slab, handed-back roots
+    DevBuf<int32_t> ck_keys, ck_vals, ck_keys2, ck_vals2, ck_slab, ck_over;
+    DevBuf<uint8_t> ck_tmp;
+    DevBuf<unsigned long long> ck_bucket, ck_sched;
+    DevBuf<int> ck_dmax;
     Workspace() : lv(kMaxK + 1) {
         for (auto& p : lv) p.reset(new LevelBufs());
     }

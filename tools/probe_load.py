@@ -12,7 +12,12 @@ for it in range(4):
     torch.cuda.synchronize(); t = time.perf_counter()
     G = gsm.gsm_load_graph(g.num_nodes, off_h, cols_h, lab_h, device=0)
     torch.cuda.synchronize(); dt = time.perf_counter() - t
-    q = w.queries[0]
-    r = gsm.gsm_match(G, q.num_nodes, q.edges, q.labels)
-    print(f"load {dt*1e3:.1f} ms; {q.name} count {r.count}", flush=True)
+    msg = []
+    for q in w.queries:
+        t = time.perf_counter()
+        r = gsm.gsm_match(G, q.num_nodes, q.edges, q.labels, mem_budget_bytes=w.mem_budget_bytes)
+        msg.append(f"{q.name} {r.count} {(time.perf_counter() - t) * 1e3:.1f} ms")
+    t = time.perf_counter()
     G.free()
+    torch.cuda.synchronize()
+    print(f"load {dt*1e3:.1f} ms; " + "; ".join(msg) + f"; free {(time.perf_counter() - t) * 1e3:.1f} ms", flush=True)

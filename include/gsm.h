@@ -131,7 +131,10 @@ enum {
     /* test-only: search all embeddings directly, without ID constraints */
     GSM_FLAG_NO_SYMMETRY = 2u,
     /* record per-kernel CUDA-event times and algorithmic-byte counters in gsm_result.prof */
-    GSM_FLAG_PROFILE = 4u
+    GSM_FLAG_PROFILE = 4u,
+    /* gsm_plan_query only: plan as a COUNT-mode match does — the two last positions an
+       independent pair of non-adjacent query vertices when Q allows it */
+    GSM_FLAG_PLAN_COUNT = 8u
 };
 
 typedef struct {

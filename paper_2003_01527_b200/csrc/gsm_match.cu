@@ -889,6 +889,7 @@ gsm_status gsm_plan_query(const gsm_query* q, const uint64_t* cand, uint32_t fla
         }
         gsm::compute_symmetry(&plan, !(flags & GSM_FLAG_NO_SYMMETRY), 0);
         gsm::compute_order(&plan, cand, -1);
+        if (flags & GSM_FLAG_PLAN_COUNT) gsm::compute_order_pair_tail(&plan, cand);
         out->k = plan.k;
         for (int i = 0; i < plan.k; ++i) {
             out->order[i] = plan.order[i];

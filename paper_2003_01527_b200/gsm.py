@@ -27,6 +27,7 @@ GSM_MODE_ENUMERATE = 1
 GSM_FLAG_UNIQUE = 1
 GSM_FLAG_NO_SYMMETRY = 2
 GSM_FLAG_PROFILE = 4
+GSM_FLAG_PLAN_COUNT = 8
 KERNEL_NAMES = ["filter", "roots", "plan", "scan", "expand", "finalize", "tail", "clique"]
 
 

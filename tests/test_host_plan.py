@@ -126,3 +126,51 @@ def test_large_symmetric_query_group_order():
     # K_8: |Aut| = 8! without listing; star K_{1,7}: 7!
     assert gsm.gsm_plan_query(8, list(itertools.combinations(range(8), 2)))["automorphisms"] == 40320
     assert gsm.gsm_plan_query(8, [(0, i) for i in range(1, 8)])["automorphisms"] == 5040
+
+
+def _pair_expected(q, conds):
+    """Brute force: does Q have non-adjacent a, b with no condition between them and
+    Q - {a, b} connected?  (the pair-tail eligibility)"""
+    k = q.num_nodes
+    adj = {u: set() for u in range(k)}
+    for a, b in q.edges:
+        adj[a].add(b)
+        adj[b].add(a)
+    for a in range(k):
+        for b in range(a + 1, k):
+            if b in adj[a] or (a, b) in conds or (b, a) in conds:
+                continue
+            rest = [u for u in range(k) if u not in (a, b)]
+            seen, stack = {rest[0]}, [rest[0]]
+            while stack:
+                x = stack.pop()
+                for y in adj[x]:
+                    if y in rest and y not in seen:
+                        seen.add(y)
+                        stack.append(y)
+            if len(seen) == len(rest):
+                return True
+    return False
+
+
+@pytest.mark.parametrize("key", ["P3", "P4", "S3", "C4", "K4", "house", "tailed_triangle", "diamond", "K3"])
+@pytest.mark.parametrize("labels", [None, "distinct"])
+def test_count_mode_pair_tail_order(key, labels):
+    """GSM_FLAG_PLAN_COUNT: when Q allows it the last two positions are non-adjacent, carry no
+    ID condition between them, and every earlier position keeps a connected prefix; else the
+    order is the plain greedy one (cliques, C4 with its conditions)."""
+    q0 = gi.query(key)
+    q = q0 if labels is None else gi.query(key, list(range(q0.num_nodes)))
+    base = plan(q)
+    p = plan(q, flags=gsm.GSM_FLAG_PLAN_COUNT)
+    conds = set(p["conditions"])
+    assert sorted(p["order"]) == list(range(q.num_nodes))
+    for i in range(1, q.num_nodes):  # connected prefix at every position
+        assert p["backward"][i] != 0, (key, p)
+    a, b = p["order"][-2], p["order"][-1]
+    adjacent = any({a, b} == {x, y} for x, y in q.edges)
+    if _pair_expected(q, conds):
+        assert not adjacent and (a, b) not in conds and (b, a) not in conds, (key, p)
+        assert not (p["backward"][-1] >> (q.num_nodes - 2)) & 1
+    else:
+        assert p["order"] == base["order"], (key, p, base)

@@ -4,14 +4,16 @@ query ms at 1/2/4/8 B200; achieved HBM GB/s vs peak).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload rmat24] [--impl ours|reference]
 
-A step = one pass of the whole hot path over the workload: gsm_match (COUNT,
-all embeddings) of every query of the workload on the resident data graph
+A step = one pass of the whole hot path over the workload: gsm_match (COUNT)
+of every query of the workload on the resident data graph
 (filter -> roots -> per-position plan/scan/partition/expand -> count).  Default
 workload = BASELINE configs[4] (R-MAT-24, K3 + K4, chunked frontier), the
 configuration the metric is quoted on at 1/2/4/8 GPUs.  Multi-GPU: one process
 per GPU (torchrun), data graph replicated (each rank regenerates it), root
 candidates sharded round-robin by (degree, id) rank, one NCCL all-reduce of
-the counts per step; time = max over ranks.
+the counts per step (inside the timed region); time = max over ranks.
+value = UNIQUE embeddings/s (one per Aut(Q) orbit — what the kernels search for;
+the all-embeddings figure |Aut(Q)| x unique is reported as all_per_s).
 
 --impl reference: the CPU oracle (oracle/, plain DFS) timed on this host's
 cores on a bounded root sample of the same workload (rank 0 only).
@@ -172,37 +174,61 @@ def ncu_traffic(workload: str, kind: str, launches_per_step: float):
 
 
 # ----------------------------------------------------------------------------- oracle baseline
-def oracle_sample(g, queries, budget_s: float, rank_roots=None):
-    """Calibrate an evenly strided root sample so the oracle spends ~budget_s seconds;
-    returns (roots, embeddings, seconds, threads).  All embeddings with f(0) in roots."""
-    import numpy as np
-    import oracle
+METRIC = "embeddings/s (unique: one per Aut(Q) orbit, i.e. per matched subgraph)"
 
+
+def strided_roots(n: int, count: int):
+    import numpy as np
+    count = max(1, min(n, int(count)))
+    stride = n / count
+    return np.unique((np.arange(count) * stride + stride / 2).astype(np.int64).clip(0, n - 1)).astype(np.int32)
+
+
+def oracle_pass(g, queries, roots):
+    """One oracle pass (plain DFS, all embeddings with f(query vertex 0) in roots) over the
+    workload's queries; returns (unique-equivalent embeddings = sum all/|Aut(Q)|, seconds)."""
+    import oracle
+    t0 = time.perf_counter()
+    uni = 0.0
+    for q in queries:
+        c = oracle.match(g, q, roots=roots, count_only=True)[0]
+        uni += c / len(oracle.automorphisms(q))
+    return uni, time.perf_counter() - t0
+
+
+def oracle_sample(g, queries, target_s: float):
+    """A FIXED evenly strided root sample sized so one oracle pass takes about target_s
+    seconds: start at 16 roots, grow geometrically while a pass is < target/3, shrink if a
+    pass overshoots 1.5 x target.  Every calibration pass is bounded by ~1.5 x target, so
+    the whole calibration costs a few targets.  Returns (roots, unique, seconds, threads)."""
+    import oracle
     n = g.num_nodes
-    stride = max(1, n // 64)
-    while True:
-        roots = np.arange(stride // 2, n, stride, dtype=np.int32)
-        t0 = time.perf_counter()
-        tot = 0
-        for q in queries:
-            tot += oracle.match(g, q, roots=roots, count_only=True)[0]
-        dt = time.perf_counter() - t0
-        if dt >= budget_s / 4 or stride == 1:
-            if dt < budget_s / 2 and stride > 1:
-                stride = max(1, int(stride * dt / budget_s))
-                continue
-            return roots, tot, dt, oracle.num_threads()
-        stride = max(1, stride // 8 if dt < budget_s / 64 else stride // 2)
+    cnt = 16
+    for _ in range(12):
+        roots = strided_roots(n, cnt)
+        uni, dt = oracle_pass(g, queries, roots)
+        if dt > 1.5 * target_s and cnt > 1:
+            cnt = max(1, int(cnt * target_s / dt))
+            continue
+        if dt < target_s / 3 and cnt < n:
+            cnt = min(n, int(cnt * min(8.0, max(1.5, 0.9 * target_s / max(dt, 1e-4)))))
+            continue
+        break
+    return roots, uni, dt, oracle.num_threads()
 
 
 def cpu_baseline(g, w, budget_s):
-    roots, tot, dt, threads = oracle_sample(g, w.queries, budget_s)
-    return {"value": tot / dt if dt > 0 else None, "unit": "embeddings/s", "cores": threads, "kind": "oracle",
-            "sample": f"all embeddings of {[q.name for q in w.queries]} with f(query vertex 0) in an evenly strided "
-                      f"sample of {len(roots)} of {g.num_nodes} vertices; {tot} embeddings in {dt:.2f} s"}
+    roots, uni, dt, threads = oracle_sample(g, w.queries, budget_s)
+    return {"value": uni / dt if dt > 0 else None, "unit": METRIC, "cores": threads, "kind": "oracle",
+            "sample": f"all embeddings of {[q.name for q in w.queries]} with f(query vertex 0) in a fixed evenly "
+                      f"strided sample of {len(roots)} of {g.num_nodes} vertices, counted as all/|Aut(Q)|; "
+                      f"{uni:.6g} unique-equivalent embeddings in {dt:.2f} s (one pass)"}
 
 
 def run_reference(args, world, rank):
+    """Reference arm = the CPU oracle as it stands (plain DFS, oracle/), rank 0 only, on a
+    fixed root sample whose per-step cost is sized so the WHOLE run (calibration, W warm-up
+    and K timed passes) stays within ~240 s whatever --steps/--warmup are."""
     import oracle  # noqa: F401  (reference arm = the CPU oracle)
     from gsm_inputs import workloads
 
@@ -210,28 +236,28 @@ def run_reference(args, world, rank):
         return
     w = workloads.get(args.workload)
     g = w.graph()
-    per_step = max(1.0, min(8.0, 120.0 / max(1, args.steps + args.warmup)))
+    per_step = max(0.3, min(8.0, 240.0 / (args.steps + args.warmup + 4)))
     roots, _, _, threads = oracle_sample(g, w.queries, per_step)
-    import oracle as O
-    for _ in range(args.warmup):
-        for q in w.queries:
-            O.match(g, q, roots=roots, count_only=True)
-    t0 = time.perf_counter()
-    tot = 0
+    for _ in range(max(0, args.warmup - 1)):  # the accepted calibration pass was one warm-up
+        oracle_pass(g, w.queries, roots)
+    tot = 0.0
+    times = []
     for _ in range(args.steps):
-        for q in w.queries:
-            tot += O.match(g, q, roots=roots, count_only=True)[0]
-    dt = time.perf_counter() - t0
+        uni, dt = oracle_pass(g, w.queries, roots)
+        tot += uni
+        times.append(dt)
+    dt = sum(times)
     value = tot / dt
-    sample = (f"all embeddings of {[q.name for q in w.queries]} with f(query vertex 0) in an evenly strided sample "
-              f"of {len(roots)} of {g.num_nodes} vertices per step")
-    out = {"impl": "reference", "metric": "embeddings/s", "value": value, "unit": "embeddings/s", "n_gpus": world,
+    sample = (f"all embeddings of {[q.name for q in w.queries]} with f(query vertex 0) in a fixed evenly strided "
+              f"sample of {len(roots)} of {g.num_nodes} vertices per step, counted as all/|Aut(Q)|")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+           "ms_median": 1000 * statistics.median(times),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
            "data": "synthetic", "config": config_of(w, g),
-           "cpu_baseline": {"value": value, "unit": "embeddings/s", "cores": threads, "kind": "oracle",
+           "cpu_baseline": {"value": value, "unit": METRIC, "cores": threads, "kind": "oracle",
                             "sample": sample},
-           "e2e": {"value": value, "unit": "embeddings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": value, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
@@ -240,7 +266,9 @@ def config_of(w, g, refine_rounds=0):
             "refine_rounds": refine_rounds,
             "graph": {"name": g.name, "num_nodes": g.num_nodes, "directed_edges": g.nnz,
                       "csr_bytes": int(g.offsets.nbytes + g.cols.nbytes + (0 if g.labels is None else g.labels.nbytes))},
-            "queries": [q.name for q in w.queries], "mode": "count, all embeddings (= |Aut(Q)| x orbit representatives)",
+            "queries": [q.name for q in w.queries],
+            "mode": "count; value = unique embeddings (one per Aut(Q) orbit, what the kernels find); "
+                    "all embeddings = |Aut(Q)| x unique in counts_per_step / all_per_s",
             "mem_budget_bytes": w.mem_budget_bytes,
             "l2": "inputs larger than L2 (no flush)" if g.offsets.nbytes + g.cols.nbytes > 126e6
                   else "graph smaller than L2: L2 flushed (256 MiB write) before every timed step"}
@@ -318,6 +346,9 @@ def run_ours(args, world, rank, local, dist):
             ev1 = torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
             c_all, c_uni, nl, profs = step(gsm.GSM_FLAG_PROFILE)
+            if dist is not None and not ONE_DEVICE:  # the step's count all-reduce (NCCL) is in the timed region
+                red = torch.tensor([c_all, c_uni], dtype=torch.int64, device=dev)
+                dist.all_reduce(red)
             ev1.record(stream)
             ev1.synchronize()
             ms_steps.append(ev0.elapsed_time(ev1))
@@ -330,12 +361,19 @@ def run_ours(args, world, rank, local, dist):
                         t[key] += d[key]
     barrier()
     ms = sum(ms_steps) / len(ms_steps)
+    ms_med = statistics.median(ms_steps)
     c_all, c_uni = counts
     cdev = "cpu" if ONE_DEVICE else dev
+    per_rank_ms = [ms]
     if dist is not None:
         t = torch.tensor([ms], dtype=torch.float64, device=cdev)
+        gathered = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        per_rank_ms = [float(x.item()) for x in gathered]
+        ms = max(per_rank_ms)
+        t = torch.tensor([ms_med], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms_med = float(t.item())
         c = torch.tensor([c_all, c_uni, launches], dtype=torch.int64, device=cdev)
         dist.all_reduce(c)
         c_all, c_uni, launches = (int(x) for x in c.tolist())
@@ -359,7 +397,7 @@ def run_ours(args, world, rank, local, dist):
         e_cnt = 0
         for _ in range(args.e2e_steps):
             G2 = gsm.gsm_load_graph(g.num_nodes, off_h, cols_h, lab_h, device=local, stream=sptr)
-            e_cnt = step(0, G2)[0]
+            e_cnt = step(0, G2)[1]
             G2.free()
         ev1.record(stream)
         ev1.synchronize()
@@ -372,7 +410,7 @@ def run_ours(args, world, rank, local, dist):
             dist.all_reduce(c)
             e_cnt = int(c.item())
         h2d = (g.offsets.nbytes + g.cols.nbytes + (0 if g.labels is None else g.labels.nbytes)) * world
-        e2e = {"value": e_cnt / (e_ms / 1000.0), "unit": "embeddings/s", "ms_per_step": e_ms,
+        e2e = {"value": e_cnt / (e_ms / 1000.0), "unit": METRIC, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * len(w.queries) * world)}
     G.free()
 
@@ -397,13 +435,15 @@ def run_ours(args, world, rank, local, dist):
             "alg_bytes_per_launch": kp["alg_bytes"] / max(1, kp["launches"]),
             "share_of_step": (kp["ms"] / args.steps) / ms if ms > 0 else None,
             "per_kernel_ms_per_step": {k: v["ms"] / args.steps for k, v in prof_tot.items()}}
-    out = {"metric": "embeddings/s", "value": c_all / (ms / 1000.0), "unit": "embeddings/s", "n_gpus": world,
+    out = {"metric": METRIC, "value": c_uni / (ms / 1000.0), "unit": METRIC, "n_gpus": world,
            **({"one_device_functional_check": True} if ONE_DEVICE else {}),
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_median": ms_med,
+           "per_rank_ms": per_rank_ms, "imbalance_max_over_mean": max(per_rank_ms) / (sum(per_rank_ms) / len(per_rank_ms)),
+           "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
            "config": config_of(w, g, args.refine_rounds),
            "counts_per_step": {"all": c_all, "unique": c_uni},
-           "unique_per_s": c_uni / (ms / 1000.0),
+           "all_per_s": c_all / (ms / 1000.0),
            "query_ms": ms, "per_query_rank0": per_query, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
     if world == 1 and not args.no_cpu_baseline:
         try:

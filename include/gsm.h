@@ -142,7 +142,10 @@ typedef struct {
     gsm_mode mode;
     uint32_t flags;           /* GSM_FLAG_* */
     int32_t shard_index;      /* root-candidate shard (multi-GPU); 0 */
-    int32_t num_shards;       /* 0 or 1 = all roots; P = keep roots with rank % P == shard_index */
+    int32_t num_shards;       /* 0 or 1 = all roots; P = keep the root candidates v whose rank in the
+                                 ascending (degree, original id) order satisfies rank % P == shard_index
+                                 (each embedding belongs to exactly one shard: the one of its root
+                                 f(π[0]); P may be as large as n, e.g. to isolate one root) */
     int32_t refine_rounds;    /* neighbourhood-encoding filter (Alg. 1 lines 7-8): 0 = label +
                                  degree only; R >= 1 = R rounds of NE(v) >= NE_Q(u), effective
                                  degree, and the 1-step look-ahead condition (every query neighbour

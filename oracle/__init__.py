@@ -67,6 +67,12 @@ def _L():
         lib.oracle_count_triangles.argtypes = [i64, p, p, ctypes.c_int]
         lib.oracle_count_k4.restype = ctypes.c_uint64
         lib.oracle_count_k4.argtypes = [i64, p, p, ctypes.c_int]
+        lib.oracle_count_triangles_roots.restype = ctypes.c_uint64
+        lib.oracle_count_triangles_roots.argtypes = [i64, p, p, p, i64, p, ctypes.c_int]
+        lib.oracle_count_k4_roots.restype = ctypes.c_uint64
+        lib.oracle_count_k4_roots.argtypes = [i64, p, p, p, i64, p, ctypes.c_int]
+        lib.oracle_count_house_roots.restype = ctypes.c_uint64
+        lib.oracle_count_house_roots.argtypes = [i64, p, p, p, p, p, i64, p, ctypes.c_int]
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -137,6 +143,58 @@ def count_triangles(graph, threads: int = 0) -> int:
 def count_k4(graph, threads: int = 0) -> int:
     """Exact number of (unlabeled) 4-cliques; all K4 embeddings = 24 * this."""
     return int(_L().oracle_count_k4(graph.num_nodes, _p(graph.offsets), _p(graph.cols), threads))
+
+
+def clique_counts_by_root(graph, k: int, roots: Optional[np.ndarray] = None, threads: int = 0):
+    """Per-root exact clique counts (k = 3 or 4): entry r = number of k-cliques whose
+    LOWEST vertex in the (degree, id) order is roots[r] (every vertex when ``roots`` is
+    None).  Each clique is counted at exactly one vertex, so any partition of the roots
+    sums to :func:`count_triangles` / :func:`count_k4` (shard parity).
+    Returns ``(total, per_root uint64 array)``."""
+    if k not in (3, 4):
+        raise ValueError("k must be 3 or 4")
+    rt = None if roots is None else np.ascontiguousarray(roots, dtype=np.int32)
+    nr = graph.num_nodes if rt is None else len(rt)
+    out = np.zeros(max(nr, 1), dtype=np.uint64)
+    fn = _L().oracle_count_triangles_roots if k == 3 else _L().oracle_count_k4_roots
+    total = fn(graph.num_nodes, _p(graph.offsets), _p(graph.cols), _p(rt), 0 if rt is None else len(rt), _p(out),
+               threads)
+    return int(total), out[:nr]
+
+
+def house_counts_by_root(graph, labels, roots: Optional[np.ndarray] = None, threads: int = 0):
+    """Exact count of the labeled house query (``gsm_inputs.query("house", labels)``:
+    square 0-1-2-3 + roof 4 on edge 0-1) by counting, not enumerating (oracle.c
+    ``oracle_count_house_roots``: sum over edges (f(0), f(1)) of roof choices x
+    4-path choices).  Entry r = embeddings with f(0) = roots[r] (all vertices when
+    None).  Only for label patterns where every non-adjacent pair of query vertices
+    has different labels (then injectivity is implied and the roof and the path are
+    independent): l4 not in {l0..l3}, l1 != l3, l0 != l2.  Returns (total, per_root)."""
+    l = [int(x) for x in labels]
+    if len(l) != 5 or l[4] in l[:4] or l[1] == l[3] or l[0] == l[2]:
+        raise ValueError("house counter needs l4 not in l0..l3, l1 != l3, l0 != l2")
+    if graph.labels is None:
+        raise ValueError("house counter needs a labeled graph")
+    gl = np.ascontiguousarray(graph.labels, dtype=np.uint32)
+    ql = np.ascontiguousarray(l, dtype=np.uint32)
+    rt = None if roots is None else np.ascontiguousarray(roots, dtype=np.int32)
+    nr = graph.num_nodes if rt is None else len(rt)
+    out = np.zeros(max(nr, 1), dtype=np.uint64)
+    total = _L().oracle_count_house_roots(graph.num_nodes, _p(graph.offsets), _p(graph.cols), _p(gl), _p(ql), _p(rt),
+                                          0 if rt is None else len(rt), _p(out), threads)
+    if total == 2 ** 64 - 1:
+        raise MemoryError("oracle_count_house_roots: allocation failed")
+    return int(total), out[:nr]
+
+
+def rank_order(graph) -> np.ndarray:
+    """rank[v] = position of v in ascending (degree, id) order — the strict total
+    order the clique counters orient by (SURVEY §8(c) amb. 9)."""
+    deg = np.diff(graph.offsets)
+    order = np.lexsort((np.arange(graph.num_nodes), deg))
+    rank = np.empty(graph.num_nodes, dtype=np.int64)
+    rank[order] = np.arange(graph.num_nodes)
+    return rank
 
 
 # ------------------------------------------------------------------ automorphisms

@@ -257,24 +257,40 @@ static int64_t merge_count(const int32_t* a, int64_t na, const int32_t* b, int64
     return c;
 }
 
-uint64_t oracle_count_triangles(int64_t n, const int64_t* off, const int32_t* cols, int nthreads) {
+/* roots == NULL: every vertex u; else only the cliques whose LOWEST vertex in the
+ * (degree, id) orientation is one of roots[0..nroots) — the vertex the forward
+ * algorithm counts each clique at (SURVEY §8(c) configs[4] pin (ii), root-restricted
+ * for shard parity: a clique belongs to the root shard of its lowest-ranked vertex). */
+uint64_t oracle_count_triangles_roots(int64_t n, const int64_t* off, const int32_t* cols, const int32_t* roots,
+                                      int64_t nroots, uint64_t* per_root, int nthreads) {
     or_oriented o;
     if (orient(n, off, cols, &o)) return ~0ULL;
     if (nthreads <= 0) nthreads = omp_get_max_threads();
+    const int64_t nu = roots ? nroots : n;
     uint64_t t = 0;
 #pragma omp parallel for num_threads(nthreads) schedule(dynamic, 256) reduction(+ : t)
-    for (int64_t u = 0; u < n; ++u)
+    for (int64_t r = 0; r < nu; ++r) {
+        const int64_t u = roots ? (int64_t)roots[r] : r;
+        uint64_t tu = 0;
         for (int64_t e = o.off[u]; e < o.off[u + 1]; ++e) {
             int32_t v = o.col[e];
-            t += (uint64_t)merge_count(o.col + o.off[u], o.off[u + 1] - o.off[u], o.col + o.off[v],
-                                       o.off[v + 1] - o.off[v]);
+            tu += (uint64_t)merge_count(o.col + o.off[u], o.off[u + 1] - o.off[u], o.col + o.off[v],
+                                        o.off[v + 1] - o.off[v]);
         }
+        if (per_root) per_root[r] = tu;
+        t += tu;
+    }
     free(o.off);
     free(o.col);
     return t;
 }
 
-uint64_t oracle_count_k4(int64_t n, const int64_t* off, const int32_t* cols, int nthreads) {
+uint64_t oracle_count_triangles(int64_t n, const int64_t* off, const int32_t* cols, int nthreads) {
+    return oracle_count_triangles_roots(n, off, cols, NULL, 0, NULL, nthreads);
+}
+
+uint64_t oracle_count_k4_roots(int64_t n, const int64_t* off, const int32_t* cols, const int32_t* roots,
+                               int64_t nroots, uint64_t* per_root, int nthreads) {
     or_oriented o;
     if (orient(n, off, cols, &o)) return ~0ULL;
     if (nthreads <= 0) nthreads = omp_get_max_threads();
@@ -286,7 +302,9 @@ uint64_t oracle_count_k4(int64_t n, const int64_t* off, const int32_t* cols, int
     {
         int32_t* s = (int32_t*)malloc(sizeof(int32_t) * (size_t)(maxout + 1));
 #pragma omp for schedule(dynamic, 64)
-        for (int64_t u = 0; u < n; ++u)
+        for (int64_t r = 0; r < (roots ? nroots : n); ++r) {
+            const int64_t u = roots ? (int64_t)roots[r] : r;
+            uint64_t tu = 0;
             for (int64_t e = o.off[u]; e < o.off[u + 1]; ++e) {
                 int32_t v = o.col[e];
                 /* s = N+(u) & N+(v) */
@@ -299,14 +317,103 @@ uint64_t oracle_count_k4(int64_t n, const int64_t* off, const int32_t* cols, int
                 }
                 for (int64_t x = 0; x < ns; ++x) {
                     int32_t w = s[x];
-                    total += (uint64_t)merge_count(s, ns, o.col + o.off[w], o.off[w + 1] - o.off[w]);
+                    tu += (uint64_t)merge_count(s, ns, o.col + o.off[w], o.off[w + 1] - o.off[w]);
                 }
             }
+            if (per_root) per_root[r] = tu;
+            total += tu;
+        }
         free(s);
     }
     free(o.off);
     free(o.col);
     return total;
+}
+
+uint64_t oracle_count_k4(int64_t n, const int64_t* off, const int32_t* cols, int nthreads) {
+    return oracle_count_k4_roots(n, off, cols, NULL, 0, NULL, nthreads);
+}
+
+/* ------------------------------------------------------------ labeled house counter */
+/* Exact count of the labeled house query (square 0-1-2-3 + roof 4 on edge 0-1;
+ * SURVEY §8(d) configs[3]) with f(0) restricted to roots (NULL = every vertex),
+ * per root.  Independent of the DFS: it counts instead of enumerating.
+ *
+ * For f(0) = a and f(1) = b (an edge, labels l0, l1) the remaining vertices
+ * split into the roof x = f(4) in N(a) & N(b) with label l4, and the path
+ * a - y - z - b with y = f(3) in N(a) (label l3), z = f(2) in N(b) (label l2),
+ * y ~ z.  Under the caller-checked label conditions l4 not in {l0..l3},
+ * l1 != l3, l0 != l2 every pair of query vertices is either adjacent or has
+ * different labels, so injectivity holds automatically and the two parts are
+ * independent given (a, b):
+ *     count(a) = sum_{b in N(a), L(b)=l1}  c(a,b) * p(a,b),
+ *     c(a,b)  = |{x in N(a) & N(b) : L(x) = l4}|,
+ *     p(a,b)  = sum_{z in N(b), L(z)=l2} w_a(z),   w_a(z) = |{y in N(a) & N(z) : L(y) = l3}|.
+ * w_a is accumulated once per root in a dense per-thread array (touched entries reset). */
+static int64_t merge_count_label(const int32_t* a, int64_t na, const int32_t* b, int64_t nb, const uint32_t* lab,
+                                 uint32_t want) {
+    int64_t i = 0, j = 0, c = 0;
+    while (i < na && j < nb) {
+        if (a[i] < b[j]) ++i;
+        else if (a[i] > b[j]) ++j;
+        else { c += lab[a[i]] == want; ++i; ++j; }
+    }
+    return c;
+}
+
+uint64_t oracle_count_house_roots(int64_t n, const int64_t* off, const int32_t* cols, const uint32_t* lab,
+                                  const uint32_t* ql /* 5 labels */, const int32_t* roots, int64_t nroots,
+                                  uint64_t* per_root, int nthreads) {
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+    const int64_t nu = roots ? nroots : n;
+    uint64_t total = 0;
+    int fail = 0;
+#pragma omp parallel num_threads(nthreads) reduction(+ : total)
+    {
+        int64_t* w = (int64_t*)calloc((size_t)n, sizeof(int64_t));
+        int32_t* touched = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+        if (!w || !touched) {
+#pragma omp atomic write
+            fail = 1;
+        }
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t r = 0; r < nu; ++r) {
+            if (!w || !touched) continue;
+            const int64_t a = roots ? (int64_t)roots[r] : r;
+            uint64_t ta = 0;
+            if (lab[a] == ql[0]) {
+                int64_t nt = 0;
+                for (int64_t e = off[a]; e < off[a + 1]; ++e) {  /* y = f(3) */
+                    const int32_t y = cols[e];
+                    if (lab[y] != ql[3]) continue;
+                    for (int64_t f = off[y]; f < off[y + 1]; ++f) {  /* z = f(2) candidates */
+                        const int32_t z = cols[f];
+                        if (lab[z] != ql[2]) continue;
+                        if (w[z]++ == 0) touched[nt++] = z;
+                    }
+                }
+                for (int64_t e = off[a]; e < off[a + 1]; ++e) {  /* b = f(1) */
+                    const int32_t b = cols[e];
+                    if (lab[b] != ql[1]) continue;
+                    int64_t p = 0;
+                    for (int64_t f = off[b]; f < off[b + 1]; ++f) {
+                        const int32_t z = cols[f];
+                        if (lab[z] == ql[2]) p += w[z];
+                    }
+                    if (!p) continue;
+                    const int64_t c = merge_count_label(cols + off[a], off[a + 1] - off[a], cols + off[b],
+                                                        off[b + 1] - off[b], lab, ql[4]);
+                    ta += (uint64_t)c * (uint64_t)p;
+                }
+                for (int64_t t = 0; t < nt; ++t) w[touched[t]] = 0;
+            }
+            if (per_root) per_root[r] = ta;
+            total += ta;
+        }
+        free(w);
+        free(touched);
+    }
+    return fail ? ~0ULL : total;
 }
 
 int oracle_num_threads(void) { return omp_get_max_threads(); }

@@ -141,7 +141,6 @@ struct CliqueArgs {
     int32_t dmax;           // max |N+(u)| of this launch (sizes shared memory / the slab)
     int32_t stream_max;     // row construction streams N+(S[i]) when its length <= stream_max * (#j)/32
     int32_t use_hash;       // k_clique_cta: cuckoo table of S(u) (0: rows by binary search only)
-    int32_t dbg;            // GSM_CLIQUE_DBG (timing experiments only; wrong counts): 1 = no level 3, 2 = no row writes
     int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
     unsigned long long* next;   // dynamic root scheduler
     unsigned long long* count;  // unique cliques (atomic)
@@ -410,10 +409,8 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int j0 = K == 4 ? ck_find(Tk, Tk + 2 * P, P, seed, v0) : (ck_has(Tk, P, seed, v0) ? 0 : -1);
                     const int j1 = K == 4 ? ck_find(Tk, Tk + 2 * P, P, seed, v1) : (ck_has(Tk, P, seed, v1) ? 0 : -1);
                     if (K == 4) {
-                        if (!(a.dbg & 2)) {
-                            if (j0 >= 0) atomicOr(&Ai[j0 >> 5], 1u << (j0 & 31));
-                            if (j1 >= 0) atomicOr(&Ai[j1 >> 5], 1u << (j1 & 31));
-                        }
+                        if (j0 >= 0) atomicOr(&Ai[j0 >> 5], 1u << (j0 & 31));
+                        if (j1 >= 0) atomicOr(&Ai[j1 >> 5], 1u << (j1 & 31));
                     } else {
                         cnt += (j0 >= 0) + (j1 >= 0);
                     }
@@ -458,7 +455,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 }
             }
         }
-        if (K == 3 || (a.dbg & 1)) continue;
+        if (K == 3) continue;
         __syncthreads();
         // ---- level 3: for every level-2 partial result (u, S[i], S[j]) (bit j of A[i]):
         //      |{l : A[i] bit l and A[j] bit l}| = popc over words of A[i] & A[j]
@@ -539,10 +536,7 @@ static int sm_count() {
     return sms;
 }
 
-static int use_hash() {  // GSM_CLIQUE_HASH=0: no cuckoo table (every row by binary search; tests)
-    const char* v = getenv("GSM_CLIQUE_HASH");
-    return (v && *v == '0') ? 0 : 1;
-}
+static int use_hash() { return knobs().clique_hash ? 1 : 0; }  // 0: every row by binary search (tests)
 
 static size_t cta_smem(int K, int dmax, bool global) {
     return sizeof(int32_t) * (size_t)cta_lay(K, dmax, global, use_hash() != 0).smem_ints;
@@ -552,22 +546,15 @@ constexpr size_t kSmemLim = 216 * 1024;  // dynamic; + static (8 KB queues, coun
 
 // largest |S(u)| whose whole per-root workspace fits one CTA's shared memory
 int clique_dsmem(int K) {
-    const char* v = getenv("GSM_CLIQUE_DSMEM");
     int d = 32;
     while (cta_smem(K, d + 32, false) <= kSmemLim) d += 32;
-    if (v && *v) d = std::min(d, std::max(64, atoi(v)));
+    if (knobs().clique_dsmem > 0) d = std::min(d, std::max(64, knobs().clique_dsmem));
     return d;
 }
 
-static int warp_max() {  // GSM_CLIQUE_WARP=0: no warp-per-root kernel (tests)
-    const char* v = getenv("GSM_CLIQUE_WARP");
-    return (v && *v == '0') ? 0 : 32;
-}
+static int warp_max() { return knobs().clique_warp; }  // 0: no warp-per-root kernel (tests)
 
-static int stream_max() {
-    const char* v = getenv("GSM_CLIQUE_STREAM");
-    return (v && *v) ? atoi(v) : 128;
-}
+static int stream_max() { return knobs().clique_stream; }
 
 template <int K, bool G, int NT, int MB>
 static void launch_cta_mb(CliqueArgs a, int64_t blocks, cudaStream_t s) {
@@ -585,8 +572,7 @@ static void launch_cta_mb(CliqueArgs a, int64_t blocks, cudaStream_t s) {
 // on R-MAT-24 K3+K4: capped 760 ms vs uncapped 1,110 ms per step — the rows are latency-bound)
 template <int K, bool G, int NT>
 static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
-    static const int occ = getenv("GSM_CLIQUE_OCC") ? atoi(getenv("GSM_CLIQUE_OCC")) : 1;
-    if (occ) launch_cta_mb<K, G, NT, 2048 / NT>(a, blocks, s);
+    if (knobs().clique_occ) launch_cta_mb<K, G, NT, 2048 / NT>(a, blocks, s);
     else launch_cta_mb<K, G, NT, 1>(a, blocks, s);
 }
 
@@ -607,8 +593,7 @@ static int clique_dglob(int K) {
     while (cta_smem(K, d + 256, true) <= kSmemLim &&
            (double)cta_lay(K, d + 256, true, true).slab_ints * 4.0 * 148 <= 4e9)
         d += 256;
-    const char* v = getenv("GSM_CLIQUE_DMAX");
-    if (v && *v) d = std::min(d, std::max(8, atoi(v)));
+    if (knobs().clique_dmax > 0) d = std::min(d, std::max(8, knobs().clique_dmax));
     return d;
 }
 
@@ -665,11 +650,9 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     a.up = r.up;
     a.stream_max = stream_max();
     a.use_hash = use_hash();
-    a.dbg = getenv("GSM_CLIQUE_DBG") ? atoi(getenv("GSM_CLIQUE_DBG")) : 0;
     DevBuf<unsigned long long> cyc;
     a.cyc = nullptr;
-    const char* trace = getenv("GSM_TRACE");
-    if (trace && trace[0] == '2') {
+    if (knobs().trace == 2) {
         cyc.ensure(4, s);
         GSM_CUDA(cudaMemsetAsync(cyc.p, 0, 4 * sizeof(unsigned long long), s));
         a.cyc = cyc.p;

@@ -61,6 +61,34 @@ struct HostTrace {
 };
 extern HostTrace g_trace;
 
+// ---------------------------------------------------------------- tuning switches
+// Path/tuning switches.  Read from the environment ONCE at the start of
+// every gsm_match (load_knobs) into a thread-local snapshot that every launcher reads —
+// no function-static caches, so a change between calls always takes effect.  Defaults are
+// the measured best; tests use the switches to force specific paths.  None of them skips
+// work or changes a result.
+struct Knobs {
+    int clique = 1;           // GSM_CLIQUE: 0 = cliques take the breadth-first path
+    int clique_warp = 32;     // GSM_CLIQUE_WARP: |N+(u)| edge of the warp-per-root kernel (0 = off)
+    int clique_dsmem = 0;     // GSM_CLIQUE_DSMEM: cap of the shared-memory CTA buckets (0 = max fitting)
+    int clique_dmax = 0;      // GSM_CLIQUE_DMAX: cap of the global-slab bucket (0 = max fitting)
+    int clique_stream = 128;  // GSM_CLIQUE_STREAM: stream-vs-search threshold (x/32 per remaining entry)
+    int clique_hash = 1;      // GSM_CLIQUE_HASH: 0 = rows by binary search only
+    int clique_occ = 1;       // GSM_CLIQUE_OCC: register cap for 2048 resident threads
+    int pair_tail = 1;        // GSM_PAIR_TAIL
+    int pair_thread_max = 16; // GSM_PAIR_THREAD_MAX
+    int fused_tail = 1;       // GSM_FUSED_TAIL
+    int tail_cap = 1024;      // GSM_TAIL_CAP (clamped 64..6144, even)
+    int tail_block_cap = 40960;  // GSM_TAIL_BLOCK_CAP (clamped 256..49152)
+    int tail_bratio = 100;    // GSM_TAIL_BRATIO_PCT
+    int count_walk = 1;       // GSM_COUNT_WALK
+    int expand_td = 512;      // GSM_EXPAND_TD (clamped 128..2048)
+    int expand_ilp = 1;       // GSM_EXPAND_ILP (1, 2 or 4)
+    int trace = 0;            // GSM_TRACE: 1 host trace, 2 per-phase cycle counters
+};
+void load_knobs();
+const Knobs& knobs();
+
 // ---------------------------------------------------------------- device memory
 // Stream-ordered allocations from the device's default memory pool.
 void* dev_alloc(size_t bytes, cudaStream_t s);

@@ -13,7 +13,9 @@
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -37,6 +39,37 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 void clear_error() { g_last_error.clear(); }
 
 HostTrace g_trace;
+
+static thread_local Knobs g_knobs;
+const Knobs& knobs() { return g_knobs; }
+
+static int env_or(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+
+void load_knobs() {
+    Knobs k;
+    k.clique = env_or("GSM_CLIQUE", k.clique);
+    k.clique_warp = env_or("GSM_CLIQUE_WARP", k.clique_warp) ? 32 : 0;
+    k.clique_dsmem = env_or("GSM_CLIQUE_DSMEM", 0);
+    k.clique_dmax = env_or("GSM_CLIQUE_DMAX", 0);
+    k.clique_stream = env_or("GSM_CLIQUE_STREAM", k.clique_stream);
+    k.clique_hash = env_or("GSM_CLIQUE_HASH", k.clique_hash);
+    k.clique_occ = env_or("GSM_CLIQUE_OCC", k.clique_occ);
+    k.pair_tail = env_or("GSM_PAIR_TAIL", k.pair_tail);
+    k.pair_thread_max = env_or("GSM_PAIR_THREAD_MAX", k.pair_thread_max);
+    k.fused_tail = env_or("GSM_FUSED_TAIL", k.fused_tail);
+    k.tail_cap = std::min(6144, std::max(64, env_or("GSM_TAIL_CAP", k.tail_cap))) & ~1;
+    k.tail_block_cap = std::min(48 * 1024, std::max(256, env_or("GSM_TAIL_BLOCK_CAP", k.tail_block_cap)));
+    k.tail_bratio = env_or("GSM_TAIL_BRATIO_PCT", k.tail_bratio);
+    k.count_walk = env_or("GSM_COUNT_WALK", k.count_walk);
+    k.expand_td = std::min(2048, std::max(128, env_or("GSM_EXPAND_TD", k.expand_td)));
+    const int u = env_or("GSM_EXPAND_ILP", 1);
+    k.expand_ilp = (u == 2 || u == 4) ? u : 1;
+    k.trace = env_or("GSM_TRACE", 0);
+    g_knobs = k;
+}
 
 void* dev_alloc(size_t bytes, cudaStream_t s) {
     void* p = nullptr;

@@ -51,7 +51,8 @@ void compute_order(QueryPlan* plan, const uint64_t* cand, int forced_first);
 // COUNT mode: if Q has two non-adjacent vertices a, b with no symmetry condition between
 // them and Q - {a, b} connected, order Q - {a, b} greedily and put a, b last (the "pair
 // tail": their candidate sets are independent given the rest).  Returns false otherwise.
-bool compute_order_pair_tail(QueryPlan* plan, const uint64_t* cand);
+// forced_first >= 0 keeps that query vertex at position 0 (root-subset sampling).
+bool compute_order_pair_tail(QueryPlan* plan, const uint64_t* cand, int forced_first = -1);
 
 // ----------------------------------------------------------------------------
 // Per-level device plan (Verify_Constraints at position i, Alg. 1 lines 10-14)

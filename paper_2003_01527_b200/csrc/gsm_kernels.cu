@@ -182,20 +182,23 @@ void launch_refine(const DevGraph& g, const FilterQuery& q, const int64_t* qne, 
 
 // ============================================================================
 // Roots: level-0 frontier = C(π[0]) (Alg. 1 line 11: "All-source BFS traversal
-// from c_set"), compacted in ascending (degree, id) rank; multi-GPU shards keep
-// every P-th root.  Stable two-pass block-scan compaction.
+// from c_set"), compacted in ascending (degree, id) rank; multi-GPU shard s of P
+// keeps the candidates whose vertex rank v (= relabelled id) has v % P == s
+// (strided over the degree order, so hubs spread round-robin, and
+// independent of the query).  Stable two-pass block-scan compaction.
 // ============================================================================
 constexpr int kRootItems = 8;
 constexpr int64_t kRootTile = (int64_t)kThreads * kRootItems;
 
 template <typename MaskT>
-__device__ __forceinline__ int root_flags(const MaskT* cmask, int64_t n, int bit, int64_t tile, uint32_t* flags) {
+__device__ __forceinline__ int root_flags(const MaskT* cmask, int64_t n, int bit, int shard, int nshards,
+                                          int64_t tile, uint32_t* flags) {
     const int64_t first = tile * kRootTile + (int64_t)threadIdx.x * kRootItems;
     int c = 0;
 #pragma unroll
     for (int j = 0; j < kRootItems; ++j) {
         const int64_t v = first + j;
-        const uint32_t f = (v < n) ? ((cmask[v] >> bit) & 1u) : 0u;
+        const uint32_t f = (v < n && (int32_t)v % nshards == shard) ? ((cmask[v] >> bit) & 1u) : 0u;
         flags[j] = f;
         c += f;
     }
@@ -204,11 +207,11 @@ __device__ __forceinline__ int root_flags(const MaskT* cmask, int64_t n, int bit
 
 template <typename MaskT>
 __global__ void __launch_bounds__(kThreads) k_root_count(const MaskT* __restrict__ cmask, int64_t n, int bit,
-                                                         int64_t* __restrict__ tile_counts) {
+                                                         int shard, int nshards, int64_t* __restrict__ tile_counts) {
     using BlockReduce = cub::BlockReduce<int, kThreads>;
     __shared__ typename BlockReduce::TempStorage tmp;
     uint32_t flags[kRootItems];
-    const int c = root_flags(cmask, n, bit, blockIdx.x, flags);
+    const int c = root_flags(cmask, n, bit, shard, nshards, blockIdx.x, flags);
     const int total = BlockReduce(tmp).Sum(c);
     if (threadIdx.x == 0) tile_counts[blockIdx.x] = total;
 }
@@ -220,18 +223,14 @@ __global__ void __launch_bounds__(kThreads) k_root_write(const MaskT* __restrict
     using BlockScan = cub::BlockScan<int, kThreads>;
     __shared__ typename BlockScan::TempStorage tmp;
     uint32_t flags[kRootItems];
-    const int c = root_flags(cmask, n, bit, blockIdx.x, flags);
+    const int c = root_flags(cmask, n, bit, shard, nshards, blockIdx.x, flags);
     int excl;
     BlockScan(tmp).ExclusiveSum(c, excl);
-    int64_t rank = tile_base[blockIdx.x] + excl;
+    int64_t pos = tile_base[blockIdx.x] + excl;
     const int64_t first = (int64_t)blockIdx.x * kRootTile + (int64_t)threadIdx.x * kRootItems;
 #pragma unroll
-    for (int j = 0; j < kRootItems; ++j) {
-        if (flags[j]) {
-            if (rank % nshards == shard) roots[rank / nshards] = (int32_t)(first + j);
-            ++rank;
-        }
-    }
+    for (int j = 0; j < kRootItems; ++j)
+        if (flags[j]) roots[pos++] = (int32_t)(first + j);
 }
 
 int64_t launch_roots(const DevGraph& g, const void* cmask, int mask_bytes, int bit, int shard, int nshards,
@@ -241,9 +240,9 @@ int64_t launch_roots(const DevGraph& g, const void* cmask, int mask_bytes, int b
     counts.ensure(tiles, s);
     base.ensure(tiles + 1, s);
     switch (mask_bytes) {
-        case 1: k_root_count<uint8_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint8_t*)cmask, g.n, bit, counts.p); break;
-        case 2: k_root_count<uint16_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint16_t*)cmask, g.n, bit, counts.p); break;
-        default: k_root_count<uint32_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint32_t*)cmask, g.n, bit, counts.p); break;
+        case 1: k_root_count<uint8_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint8_t*)cmask, g.n, bit, shard, nshards, counts.p); break;
+        case 2: k_root_count<uint16_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint16_t*)cmask, g.n, bit, shard, nshards, counts.p); break;
+        default: k_root_count<uint32_t><<<(unsigned)tiles, kThreads, 0, s>>>((const uint32_t*)cmask, g.n, bit, shard, nshards, counts.p); break;
     }
     GSM_LAUNCH("k_root_count");
     GSM_CUDA(cudaMemsetAsync(base.p, 0, sizeof(int64_t), s));
@@ -261,8 +260,7 @@ int64_t launch_roots(const DevGraph& g, const void* cmask, int mask_bytes, int b
     int64_t total = 0;
     GSM_CUDA(cudaMemcpyAsync(&total, base.p + tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     GSM_CUDA(cudaStreamSynchronize(s));
-    if (nshards <= 1) return total;
-    return total > shard ? (total - shard + nshards - 1) / nshards : 0;
+    return total;
 }
 
 template <typename MaskT>
@@ -470,13 +468,7 @@ __device__ __forceinline__ bool in_segment(const int32_t* __restrict__ cols, int
 }
 
 int64_t expand_tile(int width) {
-    static int td = -1;
-    if (td < 0) {
-        const char* v = getenv("GSM_EXPAND_TD");
-        td = (v && *v) ? atoi(v) : 512;
-        if (td < 128) td = 128;
-        if (td > 2048) td = 2048;
-    }
+    const int td = knobs().expand_td;
     if (width <= 4) return td;
     if (width <= 12) return std::min(td, 256);
     return 128;
@@ -742,8 +734,7 @@ constexpr int kWalkVT = 16;
 constexpr int kWalkMaxNb = 4;
 
 bool use_walk(const LevelPlan& L) {
-    const char* v = getenv("GSM_COUNT_WALK");
-    if (v && v[0] == '0') return false;
+    if (!knobs().count_walk) return false;
     return L.count_only && L.nb <= kWalkMaxNb;
 }
 
@@ -897,30 +888,16 @@ static void launch_walk_t(const ExpandArgs& a, const LevelPlan& L, cudaStream_t 
     GSM_LAUNCH("k_count_walk");
 }
 
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return (v && *v) ? atoi(v) : dflt;
-}
-
-// items carried per thread (memory-level parallelism of the membership searches)
-static int expand_ilp() {
-    static int u = -1;
-    if (u < 0) {
-        u = env_int("GSM_EXPAND_ILP", 1);  // measured: 1 beats 2/4 (issue-bound, not latency-bound)
-        if (u != 1 && u != 2 && u != 4) u = 1;
-    }
-    return u;
-}
+// items carried per thread (memory-level parallelism of the membership searches);
+// measured: 1 beats 2/4 (issue-bound, not latency-bound)
+static int expand_ilp() { return knobs().expand_ilp; }
 
 template <typename MaskT, bool kCountOnly, int U>
 static void launch_expand_u(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
     const size_t smem = ExpandSmem(a.TD, L.width, L.nb, kCountOnly).total;
-    static bool configured = false;  // per template instance
-    if (!configured) {
-        GSM_CUDA(cudaFuncSetAttribute(k_expand<MaskT, kCountOnly, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      200 * 1024));
-        configured = true;
-    }
+    // per launch: the attribute is per device, and a process may drive several devices
+    GSM_CUDA(cudaFuncSetAttribute(k_expand<MaskT, kCountOnly, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
     int dev = 0, sms = 148, per_sm = 1;
     GSM_CUDA(cudaGetDevice(&dev));
     GSM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1359,13 +1336,7 @@ void launch_tail_block(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& 
     }
 }
 
-int tail_block_cap() {  // per-CTA buffer for big rows (GSM_TAIL_BLOCK_CAP)
-    const char* v = getenv("GSM_TAIL_BLOCK_CAP");
-    int cap = (v && *v) ? atoi(v) : 40960;
-    if (cap < 256) cap = 256;
-    if (cap > 48 * 1024) cap = 48 * 1024;
-    return cap;
-}
+int tail_block_cap() { return knobs().tail_block_cap; }  // per-CTA buffer for big rows
 
 // ============================================================================
 // Pair tail (COUNT mode): the last two positions p, q are not adjacent in Q and carry
@@ -1584,18 +1555,13 @@ void sort_rows_by_len_desc(const int64_t* rlen, int64_t* idx, int64_t n, cudaStr
     GSM_CUDA(cudaMemcpyAsync(idx, v_out.p, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, s));
 }
 
-int tail_bratio() {  // phase-2 strategy, in percent: stream N(c) (B) when |N(c)| <= pct/100 x |RC part|
-    const char* v = getenv("GSM_TAIL_BRATIO_PCT");
-    return (v && *v) ? atoi(v) : 100;  // measured (R-MAT-20/24): 100 beats 200, 800, 3200
-}
+// phase-2 strategy, in percent: stream N(c) (B) when |N(c)| <= pct/100 x |RC part|
+// (measured on R-MAT-20/24: 100 beats 200, 800, 3200)
+int tail_bratio() { return knobs().tail_bratio; }
 
-int tail_cap() {  // per-warp candidate buffer; GSM_TAIL_CAP (tests force the overflow path with it)
-    const char* v = getenv("GSM_TAIL_CAP");
-    int cap = (v && *v) ? atoi(v) : 1024;
-    if (cap < 64) cap = 64;
-    if (cap > 6144) cap = 6144;
-    return cap & ~1;  // even: keeps the per-warp int64 area aligned
-}
+// per-warp candidate buffer (even: keeps the per-warp int64 area aligned); tests force the
+// overflow path with GSM_TAIL_CAP
+int tail_cap() { return knobs().tail_cap; }
 
 template <typename MaskT>
 static void launch_tail_t(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, cudaStream_t s) {

@@ -193,9 +193,9 @@ void Matcher::run() {
     // ---- query order with the exact |C(u)|
     compute_order(&plan_, cand, opts_.root_subset ? 0 : -1);
     {   // COUNT mode: order the two last positions as an independent pair when Q allows it
-        const char* env = getenv("GSM_PAIR_TAIL");
-        if (count_mode_ && !opts_.root_subset && k_ >= 3 && !(env && env[0] == '0'))
-            pair_ = compute_order_pair_tail(&plan_, cand);
+        // (under root_subset the pair keeps π[0] = query vertex 0 in front)
+        if (count_mode_ && k_ >= 3 && knobs().pair_tail)
+            pair_ = compute_order_pair_tail(&plan_, cand, opts_.root_subset ? 0 : -1);
     }
     for (int i = 0; i < k_; ++i) res_->order[i] = plan_.order[i];
     res_->num_levels = k_;
@@ -268,15 +268,19 @@ void Matcher::run() {
 
     size_t free_b = 0, total_b = 0;
     GSM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    {   // memory the stream-ordered pool holds (this graph's cached workspace included) is
-        // reusable, so the default budget stays stable across calls: min(total/4, 0.9 x available)
+    {   // allocatable = free + what the stream-ordered pool holds but nobody uses + this graph's
+        // cached frontier buffers (they are released and re-grown to the new chunk sizes);
+        // default budget = min(total/4, 0.9 x allocatable), stable across calls
         int dev = 0;
         GSM_CUDA(cudaGetDevice(&dev));
         cudaMemPool_t pool;
         GSM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-        uint64_t reserved = 0;
+        uint64_t reserved = 0, used = 0;
         GSM_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
-        const double avail = 0.9 * ((double)free_b + (double)reserved);
+        GSM_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+        double cached = 0;
+        for (int w = 2; w <= k_; ++w) cached += sizeof(int32_t) * (double)lv_[w]->rows.n;
+        const double avail = 0.9 * ((double)free_b + (double)(reserved > used ? reserved - used : 0) + cached);
         budget_ = opts_.mem_budget_bytes ? (int64_t)opts_.mem_budget_bytes
                                          : (int64_t)std::min((double)total_b / 4.0, avail);
     }
@@ -384,8 +388,7 @@ void Matcher::process(int w, const int32_t* F, int64_t R) {
 // Eligibility of the clique path: COUNT mode, K3 or K4, unlabeled, every position adjacent
 // to all earlier ones, and the symmetry conditions chain f(π[0]) ≺ ... ≺ f(π[k-1]).
 bool Matcher::clique_eligible() const {
-    const char* env = getenv("GSM_CLIQUE");
-    if (env && env[0] == '0') return false;
+    if (!knobs().clique) return false;
     if (!count_mode_ || (k_ != 3 && k_ != 4) || plan_.use_labels) return false;
     for (int i = 1; i < k_; ++i) {
         const LevelPlan& L = lplan_[i];
@@ -399,8 +402,7 @@ bool Matcher::clique_eligible() const {
 // label of π[k-2] (or Q is unlabeled); π[k-1]'s ID bounds from earlier positions
 // include π[k-2]'s (so RC(r) holds every admissible image of π[k-1]).
 bool Matcher::tail_eligible(TailArgs* ta) const {
-    const char* env = getenv("GSM_FUSED_TAIL");
-    if (env && env[0] == '0') return false;
+    if (!knobs().fused_tail) return false;
     if (!count_mode_ || k_ < 3) return false;
     const int c = k_ - 2, d = k_ - 1;
     if (plan_.backward[d] != (plan_.backward[c] | (1u << c))) return false;
@@ -458,9 +460,8 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
     ws_.sched.ensure(1, s_);
     GSM_CUDA(cudaMemsetAsync(ws_.sched.p, 0, sizeof(unsigned long long), s_));
     a.next = ws_.sched.p;
-    const char* trace = getenv("GSM_TRACE");
     DevBuf<unsigned long long> cyc;
-    if (trace && trace[0] == '2') {
+    if (knobs().trace == 2) {
         cyc.ensure(8, s_);
         GSM_CUDA(cudaMemsetAsync(cyc.p, 0, sizeof(unsigned long long) * 8, s_));
         a.cyc = cyc.p;
@@ -556,7 +557,7 @@ void Matcher::process_pair(int w, const int32_t* F, int64_t R) {
     a.next = ws_.sched.p;
     a.stats = stats_.p + 5 * kMaxK;
     // thread per row for short segments, the rest (appended to an overflow list) warp per row
-    const int thread_max = getenv("GSM_PAIR_THREAD_MAX") ? atoi(getenv("GSM_PAIR_THREAD_MAX")) : 16;  // measured: 16 ~ 64 > 0 > 256
+    const int thread_max = knobs().pair_thread_max;  // measured: 16 ~ 64 > 0 > 256
     ovf_idx_.ensure(R, s_);
     ovf_n_.ensure(1, s_);
     GSM_CUDA(cudaMemsetAsync(ovf_n_.p, 0, sizeof(unsigned long long), s_));
@@ -604,7 +605,16 @@ void Matcher::process_generic(int w, const int32_t* F, int64_t R) {
     } else {
         chunk = std::min<int64_t>(total, lv_[w + 1]->cap_rows);
         if (chunk < TD) chunk = std::min<int64_t>(total, TD);
-        lv_[w + 1]->rows.ensure((size_t)chunk * (w + 1), s_);
+        for (;;) {  // the budget is an estimate: on OOM halve this level's chunk (down to one tile)
+            try {
+                lv_[w + 1]->rows.ensure((size_t)chunk * (w + 1), s_);
+                break;
+            } catch (const Failure& f) {
+                if (f.status != GSM_ERR_OUT_OF_MEMORY || chunk <= TD) throw;
+                chunk = std::max<int64_t>(TD, chunk / 2);
+                lv_[w + 1]->cap_rows = chunk;
+            }
+        }
         lv_[w + 1]->out_count.ensure(1, s_);
     }
     chunk = std::min(chunk, total);
@@ -700,13 +710,14 @@ void Matcher::finalize() {
         src = all.p;
     }
     // 3. lexicographic sort into the library-owned result buffer
-    int32_t* out = nullptr;
-    GSM_CUDA(cudaMalloc(&out, sizeof(int32_t) * (size_t)total * k_));
+    // library-owned result rows: from the same stream-ordered pool as every other buffer
+    int32_t* out = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * (size_t)total * k_, s_));
     try {
         rec_.run(GSM_K_FINALIZE, 4, [&] { sort_rows(src, total, k_, g_.n, out, s_); });
         GSM_CUDA(cudaStreamSynchronize(s_));
     } catch (...) {
-        cudaFree(out);
+        cudaFreeAsync(out, s_);
+        cudaStreamSynchronize(s_);
         throw;
     }
     res_->rows = out;
@@ -732,6 +743,7 @@ void match_impl(const gsm_graph* gh, const gsm_query* q, const gsm_match_opts* u
     if (!opts.root_subset) opts.root_subset_len = 0;
 
     const auto t0 = Clock::now();
+    load_knobs();
     g_trace = HostTrace();
     QueryPlan plan;
     std::string msg;
@@ -764,8 +776,8 @@ void match_impl(const gsm_graph* gh, const gsm_query* q, const gsm_match_opts* u
     }
     out->ms_plan = plan_ms;
     out->ms_total += plan_ms;
-    if (const char* tr = getenv("GSM_TRACE")) {
-        if (tr[0] == '1')
+    {
+        if (knobs().trace == 1)
             std::fprintf(stderr,
                          "[gsm] k=%d count=%llu total %.1f ms (filter %.1f expand %.1f finalize %.1f) | allocs %ld "
                          "(%.2f GB, %.1f ms) syncs %ld (%.1f ms, includes kernel waits) chunks %llu\n",
@@ -810,7 +822,7 @@ gsm_status gsm_match(const gsm_graph* g, const gsm_query* q, const gsm_match_opt
 
 gsm_status gsm_result_free(gsm_result* r) {
     if (!r) return GSM_OK;
-    if (r->rows) {
+    if (r->rows) {  // pool allocation (cudaMallocAsync); cudaFree synchronises and releases it
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(r->device);

@@ -218,7 +218,7 @@ static bool connected_within(const QueryPlan& p, uint32_t mask) {
     return seen == mask;
 }
 
-bool compute_order_pair_tail(QueryPlan* plan, const uint64_t* cand) {
+bool compute_order_pair_tail(QueryPlan* plan, const uint64_t* cand, int forced_first) {
     QueryPlan& p = *plan;
     if (p.k < 3) return false;
     const uint32_t all = p.k == 32 ? 0xffffffffu : ((1u << p.k) - 1u);
@@ -227,6 +227,7 @@ bool compute_order_pair_tail(QueryPlan* plan, const uint64_t* cand) {
     for (int a = 0; a < p.k; ++a)
         for (int b = a + 1; b < p.k; ++b) {
             if (qadj(p, a, b)) continue;
+            if (a == forced_first || b == forced_first) continue;  // π[0] is pinned (root_subset)
             bool cond = false;
             for (auto& c : p.conds)
                 if ((c.first == a && c.second == b) || (c.first == b && c.second == a)) cond = true;
@@ -237,7 +238,7 @@ bool compute_order_pair_tail(QueryPlan* plan, const uint64_t* cand) {
         }
     if (ba < 0) return false;
     const int tail[2] = {ba, bb};
-    order_greedy(p, cand, -1, (1u << ba) | (1u << bb), tail, 2);
+    order_greedy(p, cand, forced_first, (1u << ba) | (1u << bb), tail, 2);
     return true;
 }
 

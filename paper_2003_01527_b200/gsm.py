@@ -129,6 +129,16 @@ def _ptr(a):
     return ctypes.c_void_p(a.ctypes.data), 0, a
 
 
+def _check_array(name, a, dtypes, length):
+    """dtype and length of a numpy array / torch tensor passed to the C ABI by pointer."""
+    dt = str(a.dtype).replace("torch.", "")
+    if dt not in dtypes:
+        raise ValueError(f"{name}: dtype {dt}, expected {' or '.join(dtypes)}")
+    n = int(a.numel()) if hasattr(a, "numel") else int(np.asarray(a).size)
+    if len(getattr(a, "shape", (n,))) != 1 or n != length:
+        raise ValueError(f"{name}: expected a 1-D array of {length} elements, got shape {tuple(a.shape)}")
+
+
 class Graph:
     """Handle returned by :func:`gsm_load_graph` (wraps ``gsm_graph*``)."""
 
@@ -151,7 +161,15 @@ class Graph:
 
 def gsm_load_graph(num_nodes: int, row_offsets, col_indices, labels=None, device: int = 0, validate: bool = False,
                    stream: Optional[int] = None) -> Graph:
-    """int64 offsets[n+1], int32 cols, optional uint32 labels; numpy/host or torch (host or CUDA)."""
+    """int64 offsets[n+1], int32 cols, optional uint32 labels; numpy/host or torch (host or CUDA).
+
+    The arrays must already have exactly these dtypes and sizes (the C ABI reads raw
+    pointers): a mismatch raises ValueError here instead of reading out of bounds."""
+    _check_array("row_offsets", row_offsets, ("int64",), int(num_nodes) + 1)
+    nnz = int(row_offsets[-1]) if int(num_nodes) >= 0 and len(row_offsets) else 0
+    _check_array("col_indices", col_indices, ("int32",), nnz)
+    if labels is not None:
+        _check_array("labels", labels, ("uint32", "int32"), int(num_nodes))
     ro, od1, k1 = _ptr(row_offsets)
     co, od2, k2 = _ptr(col_indices)
     lo, od3, k3 = _ptr(labels)

@@ -117,17 +117,59 @@ def _root_sample(g, label, n_uniform, seed, n_high=16):
     return np.unique(np.concatenate([uni, hi])).astype(np.int32)
 
 
+def _hubs(g, label, n):
+    """The n highest-degree vertices (carrying `label` when given)."""
+    cand = np.nonzero(g.labels == label)[0] if label is not None else np.arange(g.num_nodes)
+    deg = np.diff(g.offsets)[cand]
+    return cand[np.argsort(-deg, kind="stable")[:n]].astype(np.int32)
+
+
 @pytest.mark.parametrize("qi", [0, 1])
-def test_config3_rmat22_house(rmat22, qi):
+def test_config3_rmat22_house_exact_full_scale(rmat22, qi):
+    """configs[3] at full scale against the oracle's independent house counter (counts
+    roof x 4-path choices per edge; oracle.house_counts_by_root): the production COUNT
+    path (symmetric search + pair tail, k_pair) must give the exact total."""
     w, g, G = rmat22
     q = w.queries[qi]
+    total, _ = oracle.house_counts_by_root(g, q.labels)
     c_all, _, r = run(G, q, "count")
+    assert r.prof["tail"]["launches"] > 0, "pair tail (k_pair) did not run"
+    assert c_all == total, (q.name, c_all, total)
     c_uni, _, ru = run(G, q, "count", flags=gsm.GSM_FLAG_UNIQUE)
     c_direct, _, _ = run(G, q, "count", flags=gsm.GSM_FLAG_NO_SYMMETRY)
     aut = oracle.automorphisms(q)
     assert r.automorphisms == len(aut)
     assert c_all == len(aut) * c_uni == c_direct
-    assert c_all > 0
+
+
+@pytest.mark.parametrize("qi", [0, 1])
+def test_config3_rmat22_house_roots_with_pair_tail(rmat22, qi):
+    """Root-sampled parity of the pair-tail kernel (k_pair) at full scale: 4,096 uniform
+    label-matching roots + the 64 highest-degree label-matching roots (SURVEY §8(c) pin
+    (i)), per-root counts from the oracle's house counter.  root_subset pins π[0] = 0 and
+    keeps the pair tail on (the pair is chosen among the other vertices)."""
+    w, g, G = rmat22
+    q = w.queries[qi]
+    rng = np.random.default_rng(100 + qi)
+    cand = np.nonzero(g.labels == q.labels[0])[0]
+    uni = np.sort(rng.choice(cand, size=4096, replace=False)).astype(np.int32)
+    hubs = _hubs(g, q.labels[0], 64)
+    for roots, what in ((uni, "4096 uniform roots"), (hubs, "64 hubs")):
+        total, per = oracle.house_counts_by_root(g, q.labels, roots)
+        c, _, r = run(G, q, "count", root_subset=roots)
+        assert r.prof["tail"]["launches"] > 0, "pair tail (k_pair) did not run under root_subset"
+        assert r.order[0] == 0
+        assert c == total, (q.name, what, c, total)
+    for h in hubs[:8]:  # the largest hubs one by one
+        total, _ = oracle.house_counts_by_root(g, q.labels, np.array([h], dtype=np.int32))
+        assert run(G, q, "count", root_subset=[h])[0] == total, (q.name, int(h))
+
+
+@pytest.mark.parametrize("qi", [0, 1])
+def test_config3_rmat22_house_enumerate_sample(rmat22, qi):
+    """Sorted row lists of a root sample against the plain DFS oracle (ENUMERATE path)."""
+    w, g, G = rmat22
+    q = w.queries[qi]
     roots = _root_sample(g, q.labels[0], 1024, 7 + qi, n_high=4)  # bounded oracle time (~minutes)
     cnt, ref = oracle.match(g, q, roots=roots)
     c, rows, _ = run(G, q, "enumerate", root_subset=roots)
@@ -144,25 +186,51 @@ def rmat24():
     G.free()
 
 
-def test_config4_rmat24_triangles_exact(rmat24):
+def _golden24():
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "rmat24_cliques.json")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/rmat24_cliques.json absent (tools/make_golden_cliques.py --scale 24)")
+    return json.load(open(path))
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_config4_rmat24_cliques_exact(rmat24, k):
+    """configs[4] at full scale: the clique kernels' counts equal the oracle's independent
+    degree-ordered counter (tests/golden/rmat24_cliques.json, written by
+    tools/make_golden_cliques.py, which calls only oracle/) — total, every shard of P = 64
+    (root rank % 64), and the 64 largest hubs + 256 strided vertices one root at a time
+    (num_shards = n isolates one root)."""
     w, g, G = rmat24
-    q = gi.query("K3")
+    gold = _golden24()
+    if f"K{k}" not in gold:
+        pytest.skip(f"golden K{k} not computed yet")
+    gk = gold[f"K{k}"]
+    assert gold["num_nodes"] == g.num_nodes and gold["nnz"] == g.nnz
+    q = gi.query(f"K{k}")
+    fact = 6 if k == 3 else 24
     c, _, r = run(G, q, "count", mem_budget_bytes=w.mem_budget_bytes)
-    T = oracle.count_triangles(g)
-    assert c == 6 * T
-    # shard invariance: 4 shards sequentially on one GPU
-    tot = sum(run(G, q, "count", shard_index=s, num_shards=4, mem_budget_bytes=w.mem_budget_bytes)[0]
-              for s in range(4))
-    assert tot == c
+    assert r.prof["clique"]["launches"] > 0
+    assert c == fact * gk["total"], (c, fact * gk["total"])
+    P = 64
+    for s in range(P):
+        cs, _, _ = run(G, q, "count", shard_index=s, num_shards=P, mem_budget_bytes=w.mem_budget_bytes)
+        assert cs == fact * gk["shards"][str(P)][s], ("shard", s)
+    rank = oracle.rank_order(g)
+    n = g.num_nodes
+    for v, want in gk["roots"].items():
+        cv, _, rv = run(G, q, "count", flags=gsm.GSM_FLAG_UNIQUE, shard_index=int(rank[int(v)]), num_shards=n)
+        assert cv == want, ("root", v, cv, want)
 
 
-def test_config4_rmat24_k4_sampled_and_identities(rmat24, monkeypatch):
+def test_config4_rmat24_k4_chunked_bfs_and_samples(rmat24, monkeypatch):
+    """The north_star's breadth-first path (GSM_CLIQUE=0: chunked frontier under the fixed
+    16 GiB budget) on the same graph, and root-sampled sorted-row parity vs the DFS oracle."""
     w, g, G = rmat24
     q = gi.query("K4")
     c_all, _, r = run(G, q, "count", mem_budget_bytes=w.mem_budget_bytes)  # clique bitmap path
     assert c_all == 24 * r.count_unique and c_all > 0
-    assert r.prof["clique"]["launches"] > 0
-    # the breadth-first path (fused tail) under the fixed budget: chunked frontier, same count
     monkeypatch.setenv("GSM_CLIQUE", "0")
     c_bfs, _, r2 = run(G, q, "count", mem_budget_bytes=w.mem_budget_bytes)
     monkeypatch.delenv("GSM_CLIQUE")

@@ -248,6 +248,82 @@ def test_clique_counters_against_dfs():
     assert oracle.count_k4(gi.complete(9)) == 126
 
 
+def test_clique_counts_by_root_against_networkx():
+    """Per-root clique counts (each clique counted at its lowest (degree, id)-ranked
+    vertex) against networkx's clique enumeration — an implementation that shares
+    nothing with the merge-based forward counter — and partition sums = totals."""
+    import networkx as nx
+    for g in [gi.rmat(9, 8, seed=4), gi.random_gnp(50, 1, 3, 9), gi.grid(12, 12, seed=3), gi.complete(7)]:
+        rank = oracle.rank_order(g)
+        deg = np.diff(g.offsets)
+        # rank = position in sorted (deg, id) order, written out directly
+        by = sorted(range(g.num_nodes), key=lambda v: (int(deg[v]), v))
+        assert [int(rank[v]) for v in by] == list(range(g.num_nodes))
+        G = _nx(g)
+        for k in (3, 4):
+            want = np.zeros(g.num_nodes, dtype=np.int64)
+            for c in nx.enumerate_all_cliques(G):
+                if len(c) == k:
+                    want[min(c, key=lambda v: rank[v])] += 1
+                elif len(c) > k:
+                    break
+            total, per = oracle.clique_counts_by_root(g, k)
+            np.testing.assert_array_equal(per.astype(np.int64), want)
+            assert total == int(want.sum()) == (oracle.count_triangles(g) if k == 3 else oracle.count_k4(g))
+            sub = np.arange(1, g.num_nodes, 3, dtype=np.int32)
+            t2, p2 = oracle.clique_counts_by_root(g, k, sub)
+            np.testing.assert_array_equal(p2.astype(np.int64), want[sub])
+            assert t2 == int(want[sub].sum())
+
+
+def test_house_counter_against_dfs_and_brute_force():
+    """The counting house oracle (roof x 4-path per edge) equals the DFS oracle's count,
+    per root, on labeled graphs where every label condition holds, and brute force on tiny
+    ones; patterns that would need explicit injectivity checks are refused."""
+    cases = [(gi.rmat(10, 8, seed=5), 5, [0, 1, 2, 3, 4]), (gi.rmat(10, 8, seed=6), 3, [0, 0, 1, 1, 2]),
+             (gi.random_gnp(80, 1, 4, 3), 4, [1, 0, 3, 2, 0]),  # l4 clash -> refused
+             (gi.random_gnp(80, 1, 3, 4), 6, [2, 5, 1, 0, 3]), (gi.complete(9), 3, [0, 0, 1, 1, 2])]
+    checked = 0
+    for g0, L, labs in cases:
+        g = g0.with_labels(gi.uniform_labels(g0.num_nodes, L, 7))
+        if labs[4] in labs[:4]:
+            with pytest.raises(ValueError):
+                oracle.house_counts_by_root(g, labs)
+            continue
+        q = gi.query("house", labs)
+        total, per = oracle.house_counts_by_root(g, labs)
+        assert total == oracle.match(g, q, count_only=True)[0]
+        roots = np.arange(0, g.num_nodes, 7, dtype=np.int32)
+        t2, p2 = oracle.house_counts_by_root(g, labs, roots)
+        assert t2 == oracle.match(g, q, roots=roots, count_only=True)[0]
+        for v, c in zip(roots[:12], p2[:12]):
+            assert c == oracle.match(g, q, roots=np.array([v], np.int32), count_only=True)[0]
+        checked += 1
+    assert checked >= 3
+    for seed in range(6):  # brute force on tiny labeled graphs
+        g = gi.random_gnp(8, 1, 2, 20 + seed).with_labels(gi.uniform_labels(8, 3, seed))
+        labs = [0, 0, 1, 1, 2]
+        assert oracle.house_counts_by_root(g, labs)[0] == len(oracle.brute_force(g, gi.query("house", labs)))
+    with pytest.raises(ValueError):
+        oracle.house_counts_by_root(gi.complete(6).with_labels(np.zeros(6, np.uint32)), [0, 1, 0, 1, 2])
+
+
+@pytest.mark.parametrize("k,top", [(3, 1000), (4, 1 << 30), (2, -1)])
+def test_sort_rows_against_python_sorted(k, top):
+    """oracle.sort_rows = Python's sorted() on the rows as unsigned tuples (both of its
+    branches: one packed 64-bit key when it fits, np.lexsort otherwise; negative int32
+    values order as large unsigned ones)."""
+    rng = np.random.default_rng(k)
+    if top < 0:
+        rows = rng.integers(-2**31, 2**31, size=(3000, k), dtype=np.int64).astype(np.int32)
+    else:
+        rows = rng.integers(0, top, size=(3000, k)).astype(np.int32)
+    rows[100:200] = rows[0:100]  # ties
+    got = oracle.sort_rows(rows)
+    want = sorted((tuple(int(x) & 0xffffffff for x in r) for r in rows))
+    assert [tuple(int(x) & 0xffffffff for x in r) for r in got] == want
+
+
 # ------------------------------------------------------------------ restriction / invariance
 def test_root_subset_partition_union():
     g = gi.rmat(9, 8, seed=2).with_labels(gi.uniform_labels(512, 2, 2))

@@ -303,6 +303,35 @@ def petersen() -> Graph:
     return from_edge_list(10, outer + spokes + inner, "petersen")
 
 
+def chain_with_tails(num_chains: int, length: int, seed: int = 1, tail_percent: int = 50) -> Graph:
+    """Road-like sparse graph ("chain-with-tails", mimicking road_central's
+    low average degree): num_chains disjoint paths of `length` vertices, each
+    chain vertex carrying a pendant degree-1 tail with probability tail_percent %, and
+    consecutive chains joined end to end with probability 1/2 (longer roads)."""
+    src, dst = [], []
+    n = 0
+    prev_end = -1
+    thr = _threshold(tail_percent)
+    for c in range(num_chains):
+        first = n
+        for i in range(length):
+            v = n
+            n += 1
+            if i:
+                src.append(v - 1)
+                dst.append(v)
+        if prev_end >= 0 and (draw(seed, 0x4a4f494e, c) & 1):
+            src.append(prev_end)
+            dst.append(first)
+        prev_end = n - 1
+        for i in range(length):
+            if (draw(seed, 0x5441494c, first + i) & 0xffffffff) < thr:
+                src.append(first + i)
+                dst.append(n)
+                n += 1
+    return csr_from_edges(n, np.asarray(src, np.int32), np.asarray(dst, np.int32), f"chain-tails-{num_chains}x{length}")
+
+
 def plain_grid(W: int, H: int) -> Graph:
     e = []
     for y in range(H):

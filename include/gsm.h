@@ -134,7 +134,11 @@ enum {
     GSM_FLAG_PROFILE = 4u,
     /* gsm_plan_query only: plan as a COUNT-mode match does — the two last positions an
        independent pair of non-adjacent query vertices when Q allows it */
-    GSM_FLAG_PLAN_COUNT = 8u
+    GSM_FLAG_PLAN_COUNT = 8u,
+    /* store intermediate partial results as level-wise (parent row, vertex) pairs — 8 bytes per
+       partial result at any width instead of 4 x width (PAPER P:136/"store the value
+       to partial results ... to further save memory usage"; bijective, so listings are exact) */
+    GSM_FLAG_COMPRESSED_PARTIALS = 16u
 };
 
 typedef struct {
@@ -152,6 +156,14 @@ typedef struct {
                                  of u has a candidate among v's neighbours), each
                                  recomputed over the surviving vertices.  Sound: never changes the
                                  result, only the candidate sets. */
+    int32_t lookahead;        /* k-look-ahead in the verification step (§3.3, Table 2;
+                                 SPEC S:225-233): 0 = off; 1 = a new partial result whose image v of
+                                 π[i] has, for some unmapped query neighbour u' of π[i], no neighbour
+                                 left that can host u' (|N(v) ∩ C(u')| minus the mapped ones known to
+                                 be there) is dropped; 2 = additionally such a neighbour must itself
+                                 have a candidate neighbour for each later query neighbour of u'.
+                                 Necessary conditions only: never changes the result, only the
+                                 intermediate rows (level_rows) — DESIGN.md reading R17. */
     const int32_t* root_subset; /* HOST, optional (test/parity sampling): only embeddings with
                                    f(query vertex 0) in the subset (original ids).  Forces the
                                    query order to start at vertex 0 and implies NO_SYMMETRY. */
@@ -203,6 +215,9 @@ typedef struct {
     gsm_kernel_prof prof[GSM_K_COUNT_];
     int32_t device;
     int32_t symmetric;       /* 1 if ID constraints were used */
+    uint64_t level_frontier_bytes[GSM_MAX_QUERY_NODES]; /* bytes of the stored partial results of each
+                                width w = i+1 (summed over chunks; plain 4w, compressed 8 per row) */
+    int32_t compressed;      /* 1 if intermediate partial results used the compressed layout */
 } gsm_result;
 
 /*
@@ -250,6 +265,17 @@ GSM_API gsm_status gsm_plan_query(const gsm_query* q, const uint64_t* cand, uint
  */
 GSM_API gsm_status gsm_sort_rows(int32_t* rows, uint64_t num_rows, int32_t width, int64_t max_id, int32_t device,
                                  void* stream);
+
+/*
+ * gsm_filter_candidates — the candidate filter alone (Alg. 1 lines 6-9, PAPER P:108-110,
+ * P:129): out[v] for every data vertex v (ORIGINAL id order) = bitmask of the query
+ * vertices u with v in C(u): label(v) = label_Q(u) and deg(v) >= deg_Q(u), then
+ * refine_rounds rounds of the NE / effective-degree refinement exactly as gsm_match uses them.
+ *   out            uint32[n]: host memory (out_on_device = 0) or device memory on g's device.
+ * Errors as gsm_match (invalid query, labels on an unlabeled graph, no device).
+ */
+GSM_API gsm_status gsm_filter_candidates(const gsm_graph* g, const gsm_query* q, int32_t refine_rounds,
+                                         uint32_t* out, int32_t out_on_device);
 
 /* Thread-local message for the last non-OK status ("" if none). */
 GSM_API const char* gsm_last_error(void);

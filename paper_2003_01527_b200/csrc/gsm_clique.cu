@@ -141,6 +141,10 @@ struct CliqueArgs {
     int32_t dmax;           // max |N+(u)| of this launch (sizes shared memory / the slab)
     int32_t stream_max;     // row construction streams N+(S[i]) when its length <= stream_max * (#j)/32
     int32_t use_hash;       // k_clique_cta: cuckoo table of S(u) (0: rows by binary search only)
+    const uint32_t* hub_bits;  // hub adjacency bitmap (DevGraph::hub_bits) or nullptr
+    int32_t hub_base;       // first hub rank
+    int32_t hub_words;      // H / 32
+    int32_t hub_ratio;      // k_clique_cta: a hub row takes bitmap lookups when 32 nj <= hub_ratio |N+(a)|
     int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
     unsigned long long* next;   // dynamic root scheduler
     unsigned long long* count;  // unique cliques (atomic)
@@ -173,7 +177,18 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
             const int64_t ls = a.off[ai] + a.up[ai], le = a.off[ai + 1];
             const int nj = d - 1 - i;
             unsigned bits = 0;
-            if (le - ls <= (int64_t)a.stream_max) {
+            if (a.hub_bits && ai >= a.hub_base) {
+                // hub pivot: S[j] > S[i] >= hub_base, one bitmap word per lane (L2-resident)
+                const uint32_t* hr = hub_row(a.hub_bits, a.hub_words, ai - a.hub_base);
+                const bool live = lane > i && lane < d;
+                bool f = false;
+                if (live) {
+                    const int c = sv - a.hub_base;
+                    f = (__ldg(hr + (c >> 5)) >> (c & 31)) & 1u;
+                }
+                bits = __ballot_sync(kFull, f);
+                items += live;
+            } else if (le - ls <= (int64_t)a.stream_max) {
                 // stream N+(S[i]); each entry looked up in S[i+1, d) (shared memory)
                 for (int64_t x0 = ls; x0 < le; x0 += 32) {
                     const int64_t x = x0 + lane;
@@ -393,6 +408,34 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             const int len = RL[i];
             const int64_t le = ls + len;
             const int nj = d - 1 - i;
+            const int32_t ai = S[i];
+            if (a.hub_bits && ai >= a.hub_base && 32LL * nj <= (int64_t)a.hub_ratio * len) {
+                // hub pivot: every S[j] (j > i) is a hub too; bit j of A[i] = one word of the
+                // L2-resident hub bitmap row of S[i] (replaces the stream / binary search)
+                const uint32_t* hr = hub_row(a.hub_bits, a.hub_words, ai - a.hub_base);
+                for (int w = w0; w < W; ++w) {
+                    const int j = (w << 5) + lane;
+                    const bool live = j > i && j < d;
+                    bool f = false;
+                    if (live) {
+                        const int c = S[j] - a.hub_base;
+                        f = (__ldg(hr + (c >> 5)) >> (c & 31)) & 1u;
+                    }
+                    items += live;
+                    const unsigned bits = __ballot_sync(kFull, f);
+                    if (K == 4) {
+                        if (lane == 0) Ai[w] = bits;
+                    } else {
+                        cnt += f;
+                    }
+                }
+                if (a.cyc) {
+                    const long long t1 = clock64();
+                    cy[2] += t1 - tc;
+                    tc = t1;
+                }
+                continue;
+            }
             // streaming needs the cuckoo table; without it (GSM_CLIQUE_HASH=0, or 4 failed
             // builds) every row takes the binary-search strategy
             if (use_ck && (int64_t)len * 32 <= (int64_t)a.stream_max * nj) {
@@ -606,6 +649,9 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     const int dglob = clique_dglob(K);
     const int e[kNB - 1] = {warp_max(), 128, 256, 512, K == 4 ? 960 : 1024, dsmem, std::max(dsmem, dglob)};
     for (int b = 0; b < kNB - 1; ++b) E.e[b] = std::min(e[b], dglob);
+    // a lowered shared-memory cap (GSM_CLIQUE_DSMEM, tests) also caps the smaller CTA buckets,
+    // so roots above it reach the global-slab kernel
+    for (int b = 1; b <= 4; ++b) E.e[b] = std::min(E.e[b], dsmem);
     Workspace& W_ = *r.ws;  // grow-only, kept with the graph (no pool round trips per call)
     DevBuf<int32_t>&keys = W_.ck_keys, &vals = W_.ck_vals, &keys2 = W_.ck_keys2, &vals2 = W_.ck_vals2,
                    &slab = W_.ck_slab;
@@ -650,6 +696,10 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     a.up = r.up;
     a.stream_max = stream_max();
     a.use_hash = use_hash();
+    a.hub_bits = knobs().clique_hub ? r.hub_bits : nullptr;
+    a.hub_base = r.hub_base;
+    a.hub_words = r.hub_words;
+    a.hub_ratio = knobs().clique_hub_ratio;
     DevBuf<unsigned long long> cyc;
     a.cyc = nullptr;
     if (knobs().trace == 2) {

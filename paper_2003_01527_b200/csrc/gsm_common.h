@@ -29,7 +29,26 @@ struct DevGraph {
     int32_t* new2old = nullptr;   // n
     int32_t* old2new = nullptr;   // n
     int32_t max_degree = 0;
+    // Hub adjacency bitmap ("dense core"): the H highest-ranked vertices
+    // [hub_base, n) — the highest degrees — with, per hub a, the bits of N+(a) (which lies
+    // entirely inside the hub range, N+(a) ⊂ (a, n)).  Upper-triangular by 32-row blocks:
+    // row r = a - hub_base keeps words [r/32, hub_words); hub_row() gives a pointer that is
+    // indexed by the column's full word index c >> 5.  An adjacency test of two hubs is one
+    // L2-resident load instead of a binary search.  nullptr = disabled (GSM_HUB_BITS=0).
+    uint32_t* hub_bits = nullptr;
+    int32_t hub_base = 0;
+    int32_t hub_words = 0;        // H / 32
+    int64_t hub_bytes = 0;
 };
+
+// pointer p with p[c >> 5] = the word holding column c (c > r) of hub row r
+__host__ __device__ __forceinline__ const uint32_t* hub_row(const uint32_t* bits, int hw, int r) {
+    const int64_t b = r >> 5;
+    return bits + 32 * (b * hw - b * (b - 1) / 2) + (int64_t)(r & 31) * (hw - b) - b;
+}
+__host__ __device__ __forceinline__ int64_t hub_total_words(int hw) {
+    return 32 * ((int64_t)hw * hw - (int64_t)hw * (hw - 1) / 2);
+}
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
@@ -85,6 +104,11 @@ struct Knobs {
     int expand_td = 512;      // GSM_EXPAND_TD (clamped 128..2048)
     int expand_ilp = 1;       // GSM_EXPAND_ILP (1, 2 or 4)
     int trace = 0;            // GSM_TRACE: 1 host trace, 2 per-phase cycle counters
+    int compress = -1;        // GSM_COMPRESS: 1/0 force the compressed partial layout on/off (-1 = flag)
+    int lookahead = -1;       // GSM_LOOKAHEAD: overrides gsm_match_opts.lookahead when >= 0
+    int hub_bits = 32768;     // GSM_HUB_BITS: H of the hub adjacency bitmap built at load (0 = none)
+    int clique_hub = 1;       // GSM_CLIQUE_HUB: clique rows of a hub pivot by bitmap lookups
+    int clique_hub_ratio = 64;  // GSM_CLIQUE_HUB_RATIO: lookups when 32 nj <= ratio |N+(S[i])|
 };
 void load_knobs();
 const Knobs& knobs();

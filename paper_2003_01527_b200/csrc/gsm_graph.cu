@@ -68,6 +68,11 @@ void load_knobs() {
     const int u = env_or("GSM_EXPAND_ILP", 1);
     k.expand_ilp = (u == 2 || u == 4) ? u : 1;
     k.trace = env_or("GSM_TRACE", 0);
+    k.lookahead = env_or("GSM_LOOKAHEAD", -1);
+    k.compress = env_or("GSM_COMPRESS", -1);
+    k.hub_bits = std::max(0, env_or("GSM_HUB_BITS", k.hub_bits)) & ~31;
+    k.clique_hub = env_or("GSM_CLIQUE_HUB", k.clique_hub);
+    k.clique_hub_ratio = env_or("GSM_CLIQUE_HUB_RATIO", k.clique_hub_ratio);
     g_knobs = k;
 }
 
@@ -223,6 +228,21 @@ __global__ void k_permute_labels(const uint32_t* __restrict__ labels, const int3
         out[p] = labels[new2old[p]];
 }
 
+// hub bitmap: warp per hub a, one bit per entry of N+(a) (all inside the hub range)
+__global__ void k_hub_bits(const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                           const int32_t* __restrict__ up, int32_t base, int32_t H, int hw, uint32_t* bits) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < H;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t a = base + (int32_t)r;
+        uint32_t* row = const_cast<uint32_t*>(hub_row(bits, hw, (int)r));
+        for (int64_t e = off[a] + up[a] + lane; e < off[a + 1]; e += 32) {
+            const int c = cols[e] - base;
+            atomicOr(row + (c >> 5), 1u << (c & 31));
+        }
+    }
+}
+
 static int grid_for(int64_t items, int threads = 256) {
     int64_t b = (items + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -247,7 +267,7 @@ static void free_graph(gsm_graph* h) {
     // graph arrays come from the device's stream-ordered pool (kept cached by its release
     // threshold, so a load/free/load cycle does not re-map memory)
     for (void* p : {(void*)g.off, (void*)g.cols, (void*)g.up, (void*)g.labels, (void*)g.lkeys, (void*)g.new2old,
-                    (void*)g.old2new})
+                    (void*)g.old2new, (void*)g.hub_bits})
         if (p) cudaFreeAsync(p, h->stream);
     cudaStreamSynchronize(h->stream);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -259,6 +279,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
                             int32_t on_device, const gsm_load_opts* opts, gsm_graph** out) {
     if (!out) fail(GSM_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
+    load_knobs();
     if (opts && opts->struct_size != sizeof(gsm_load_opts)) fail(GSM_ERR_INVALID_ARGUMENT, "gsm_load_opts.struct_size mismatch");
     if (n <= 0) fail(GSM_ERR_INVALID_GRAPH, "graph has no vertices");
     if (n >= (int64_t)0x7fffffff) fail(GSM_ERR_INVALID_GRAPH, "more than 2^31-1 vertices");
@@ -403,6 +424,20 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
     }
     k_up<<<grid_for(n), 256, 0, s>>>(g.off, g.cols, n, g.up);
     GSM_LAUNCH("k_up");
+    // 3. hub adjacency bitmap of the H highest-ranked vertices (load-time derived data)
+    if (knobs().hub_bits > 0) {
+        const int32_t H = (int32_t)std::min<int64_t>(n, knobs().hub_bits) & ~31;
+        if (H >= 64) {
+            g.hub_base = (int32_t)(n - H);
+            g.hub_words = H / 32;
+            g.hub_bytes = 4 * hub_total_words(g.hub_words);
+            g.hub_bits = static_cast<uint32_t*>(dev_alloc((size_t)g.hub_bytes, s));
+            GSM_CUDA(cudaMemsetAsync(g.hub_bits, 0, (size_t)g.hub_bytes, s));
+            k_hub_bits<<<grid_for((int64_t)H * 32), 256, 0, s>>>(g.off, g.cols, g.up, g.hub_base, H, g.hub_words,
+                                                                 g.hub_bits);
+            GSM_LAUNCH("k_hub_bits");
+        }
+    }
     if (labels) {
         g.labels = static_cast<uint32_t*>(dev_alloc(sizeof(uint32_t) * n, s));
         k_permute_labels<<<grid_for(n), 256, 0, s>>>(d_lab, g.new2old, n, g.labels);

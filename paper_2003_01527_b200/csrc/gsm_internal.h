@@ -75,6 +75,10 @@ struct LevelPlan {
     int32_t keyed;
     int32_t key_base;
     int32_t idmask;
+    // k-look-ahead (DESIGN R17): the unmapped query neighbours of π[i]
+    int32_t la_depth;    // 0 (off), 1 or 2
+    int32_t nla;
+    int32_t la_u[kMaxK];
 };
 
 LevelPlan make_level_plan(const QueryPlan& p, int i, bool count_only);

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "gsm_kernels.h"
 
@@ -32,38 +33,83 @@ inline int grid_for(int64_t items, int threads = kThreads, int cap = kMaxGrid) {
 
 // ============================================================================
 // K1 candidate filter — Alg. 1 "Filter+Compute" (line 8), PAPER P:110, P:129,
-// compatible = same label and degree >= deg_Q(u).  Coalesced streaming
-// of offsets (8 B/vertex, each pair shared by neighbouring threads), labels
-// (4 B/vertex) and cmask writes (1-4 B/vertex).  |C(u)| via warp ballots:
-// lane u keeps popc(ballot(bit u)), one atomic per lane per warp at the end.
+// compatible = same label and degree >= deg_Q(u).  A coalesced, vectorised
+// stream: each thread owns 4 consecutive vertices — two 16-byte loads of offsets
+// (the 5th offset comes from the next lane by a shuffle), one 16-byte load of
+// labels, one 4/8/16-byte store of the 4 masks.  |C(u)| = per-thread bit counts
+// summed by one warp reduction (redux.sync) per query vertex per 128 vertices.
 // ============================================================================
+template <typename MaskT>
+struct MaskVec4;
+template <>
+struct MaskVec4<uint8_t> {
+    using T = uint32_t;
+    __device__ static T pack(const uint32_t* m) { return m[0] | (m[1] << 8) | (m[2] << 16) | (m[3] << 24); }
+};
+template <>
+struct MaskVec4<uint16_t> {
+    using T = uint2;
+    __device__ static T pack(const uint32_t* m) { return make_uint2(m[0] | (m[1] << 16), m[2] | (m[3] << 16)); }
+};
+template <>
+struct MaskVec4<uint32_t> {
+    using T = uint4;
+    __device__ static T pack(const uint32_t* m) { return make_uint4(m[0], m[1], m[2], m[3]); }
+};
+
 template <typename MaskT>
 __global__ void __launch_bounds__(kThreads) k_filter(const int64_t* __restrict__ off,
                                                      const uint32_t* __restrict__ labels, int64_t n,
                                                      FilterQuery q, MaskT* __restrict__ cmask,
                                                      unsigned long long* __restrict__ counts) {
     const int lane = threadIdx.x & 31;
-    unsigned long long mine = 0;
+    unsigned long long mine = 0;  // lane u: |C(u)| of this warp's vertices
+    const int64_t nvec = n >> 2;  // full groups of 4 vertices
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-        const int64_t v = base + threadIdx.x;
+    auto mask_of = [&](int64_t d, uint32_t lab) {
+        uint32_t m = 0;
+        for (int u = 0; u < q.k; ++u) m |= (uint32_t)((!q.use_labels || lab == q.qlabel[u]) && d >= q.qdeg[u]) << u;
+        return m;
+    };
+    // grid-stride over groups; the loop bound is warp-uniform so the shuffles stay converged
+    for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x; g0 < nvec; g0 += stride) {
+        const int64_t gi = g0 + threadIdx.x;
+        const bool live = gi < nvec;
+        int64_t o[5] = {0, 0, 0, 0, 0};
+        uint4 lab = make_uint4(0, 0, 0, 0);
+        if (live) {
+            const longlong2 a = reinterpret_cast<const longlong2*>(off)[2 * gi];
+            const longlong2 b = reinterpret_cast<const longlong2*>(off)[2 * gi + 1];
+            o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+            if (labels && q.use_labels) lab = reinterpret_cast<const uint4*>(labels)[gi];
+        }
+        const int64_t nxt = __shfl_down_sync(0xffffffffu, o[0], 1);
+        o[4] = (lane == 31 || gi + 1 >= nvec) ? (live ? off[4 * gi + 4] : 0) : nxt;
+        uint32_t m[4] = {0, 0, 0, 0};
+        if (live) {
+            m[0] = mask_of(o[1] - o[0], lab.x);
+            m[1] = mask_of(o[2] - o[1], lab.y);
+            m[2] = mask_of(o[3] - o[2], lab.z);
+            m[3] = mask_of(o[4] - o[3], lab.w);
+            reinterpret_cast<typename MaskVec4<MaskT>::T*>(cmask)[gi] = MaskVec4<MaskT>::pack(m);
+        }
+        for (int u = 0; u < q.k; ++u) {
+            const unsigned c = ((m[0] >> u) & 1u) + ((m[1] >> u) & 1u) + ((m[2] >> u) & 1u) + ((m[3] >> u) & 1u);
+            const unsigned w = __reduce_add_sync(0xffffffffu, c);
+            if (lane == u) mine += w;
+        }
+    }
+    // the last n % 4 vertices
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const int64_t v = 4 * nvec + lane;
         uint32_t m = 0;
         if (v < n) {
-            const int64_t d = off[v + 1] - off[v];
-            const uint32_t lab = labels ? labels[v] : 0u;
-#pragma unroll
-            for (int u = 0; u < kMaxK; ++u) {
-                if (u >= q.k) break;
-                const bool ok = (!q.use_labels || lab == q.qlabel[u]) && d >= q.qdeg[u];
-                m |= (uint32_t)ok << u;
-            }
+            m = mask_of(off[v + 1] - off[v], labels ? labels[v] : 0u);
             cmask[v] = (MaskT)m;
         }
-#pragma unroll
-        for (int u = 0; u < kMaxK; ++u) {
-            if (u >= q.k) break;
-            const unsigned b = __ballot_sync(0xffffffffu, (m >> u) & 1u);
-            if (lane == u) mine += __popc(b);
+        for (int u = 0; u < q.k; ++u) {
+            const unsigned w = __popc(__ballot_sync(0xffffffffu, (m >> u) & 1u));
+            if (lane == u) mine += w;
         }
     }
     if (lane < q.k && mine) atomicAdd(&counts[lane], mine);
@@ -71,13 +117,30 @@ __global__ void __launch_bounds__(kThreads) k_filter(const int64_t* __restrict__
 
 void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigned long long* counts,
                    cudaStream_t s) {
-    const int grid = grid_for(g.n);
+    // one group of 4 vertices per thread per pass; grid = SMs x resident blocks (8 x 256 threads)
+    const int grid = grid_for((g.n + 3) / 4, kThreads, 148 * 8);
     switch (mask_bytes_for(q.k)) {
         case 1: k_filter<uint8_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint8_t*)cmask, counts); break;
         case 2: k_filter<uint16_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint16_t*)cmask, counts); break;
         default: k_filter<uint32_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint32_t*)cmask, counts); break;
     }
     GSM_LAUNCH("k_filter");
+}
+
+template <typename MaskT>
+__global__ void k_mask_to_original(const MaskT* __restrict__ cmask, const int32_t* __restrict__ new2old, int64_t n,
+                                   uint32_t* __restrict__ out) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        out[new2old[v]] = (uint32_t)cmask[v];
+}
+
+void launch_mask_to_original(const DevGraph& g, const void* cmask, int mask_bytes, uint32_t* out, cudaStream_t s) {
+    switch (mask_bytes) {
+        case 1: k_mask_to_original<<<grid_for(g.n), kThreads, 0, s>>>((const uint8_t*)cmask, g.new2old, g.n, out); break;
+        case 2: k_mask_to_original<<<grid_for(g.n), kThreads, 0, s>>>((const uint16_t*)cmask, g.new2old, g.n, out); break;
+        default: k_mask_to_original<<<grid_for(g.n), kThreads, 0, s>>>((const uint32_t*)cmask, g.new2old, g.n, out); break;
+    }
+    GSM_LAUNCH("k_mask_to_original");
 }
 
 // ============================================================================
@@ -178,6 +241,75 @@ void launch_refine(const DevGraph& g, const FilterQuery& q, const int64_t* qne, 
         case 2: refine_t<uint16_t>(g, q, qne, rounds, cmask, tmp, counts, s); break;
         default: refine_t<uint32_t>(g, q, qne, rounds, cmask, tmp, counts, s); break;
     }
+}
+
+// ============================================================================
+// k-look-ahead tables (§3.3 "detect a state which won't have any
+// consistent descendants k step ahead"; R17).  Per data vertex v and query
+// vertex u: c[v][u] = |{w in N(v) : mask[w] bit u}| capped at 255 — with mask = cmask
+// this is how many neighbours of v can host u (1-step); with mask = ok1 it counts the
+// neighbours that can host u AND have a candidate neighbour for each later query
+// neighbour of u (2-step).  Warp per vertex, one ballot per query vertex per 32 entries.
+// ============================================================================
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_la_counts(const int64_t* __restrict__ off,
+                                                        const int32_t* __restrict__ cols, int64_t n, int k,
+                                                        const MaskT* __restrict__ mask, uint8_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t v = warp; v < n; v += nwarps) {
+        unsigned c = 0;  // lane u: count for query vertex u
+        for (int64_t e0 = off[v]; e0 < off[v + 1]; e0 += 32) {
+            const int64_t e = e0 + lane;
+            const uint32_t m = e < off[v + 1] ? (uint32_t)mask[cols[e]] : 0u;
+            for (int u = 0; u < k; ++u) {
+                const unsigned b = __ballot_sync(0xffffffffu, (m >> u) & 1u);
+                if (lane == u) c += __popc(b);
+            }
+            if (__all_sync(0xffffffffu, lane >= k || c >= 255)) break;
+        }
+        if (lane < k) out[v * k + lane] = (uint8_t)min(c, 255u);
+    }
+}
+
+template <typename MaskT>
+__global__ void __launch_bounds__(kThreads) k_la_ok1(const MaskT* __restrict__ cmask, const uint8_t* __restrict__ c1,
+                                                     int64_t n, int k, FilterQuery dq, MaskT* __restrict__ ok1) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n; w += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = cmask[w];
+        uint32_t have = 0;  // u'' with a candidate neighbour
+        for (int u = 0; u < k; ++u) have |= (uint32_t)(c1[w * k + u] != 0) << u;
+        uint32_t ok = 0;
+        for (int u = 0; u < k; ++u)
+            if (((m >> u) & 1u) && (dq.qadj[u] & ~have) == 0) ok |= 1u << u;
+        ok1[w] = (MaskT)ok;
+    }
+}
+
+void launch_la_counts(const DevGraph& g, int k, int mask_bytes, const void* mask, uint8_t* out, cudaStream_t s) {
+    const int grid = grid_for(g.n * 32);
+    switch (mask_bytes) {
+        case 1: k_la_counts<uint8_t><<<grid, kThreads, 0, s>>>(g.off, g.cols, g.n, k, (const uint8_t*)mask, out); break;
+        case 2: k_la_counts<uint16_t><<<grid, kThreads, 0, s>>>(g.off, g.cols, g.n, k, (const uint16_t*)mask, out); break;
+        default: k_la_counts<uint32_t><<<grid, kThreads, 0, s>>>(g.off, g.cols, g.n, k, (const uint32_t*)mask, out); break;
+    }
+    GSM_LAUNCH("k_la_counts");
+}
+
+void launch_la_ok1(const DevGraph& g, int k, int mask_bytes, const void* cmask, const uint8_t* c1,
+                   const uint32_t* dmask_host, void* ok1, cudaStream_t s) {
+    FilterQuery dq;
+    std::memset(&dq, 0, sizeof(dq));
+    dq.k = k;
+    for (int u = 0; u < k; ++u) dq.qadj[u] = dmask_host[u];
+    const int grid = grid_for(g.n);
+    switch (mask_bytes) {
+        case 1: k_la_ok1<uint8_t><<<grid, kThreads, 0, s>>>((const uint8_t*)cmask, c1, g.n, k, dq, (uint8_t*)ok1); break;
+        case 2: k_la_ok1<uint16_t><<<grid, kThreads, 0, s>>>((const uint16_t*)cmask, c1, g.n, k, dq, (uint16_t*)ok1); break;
+        default: k_la_ok1<uint32_t><<<grid, kThreads, 0, s>>>((const uint32_t*)cmask, c1, g.n, k, dq, (uint32_t*)ok1); break;
+    }
+    GSM_LAUNCH("k_la_ok1");
 }
 
 // ============================================================================
@@ -332,17 +464,17 @@ __device__ __forceinline__ void admissible_segment(const int64_t* __restrict__ o
     if (t < s) t = s;
 }
 
-__global__ void __launch_bounds__(kThreads) k_plan_rows(const int32_t* __restrict__ F, int64_t R, LevelPlan L,
+__global__ void __launch_bounds__(kThreads) k_plan_rows(const Frontier F, int64_t R, LevelPlan L,
                                                         const int64_t* __restrict__ off,
                                                         const int32_t* __restrict__ cols,
                                                         const int32_t* __restrict__ up, int64_t n,
                                                         int64_t* __restrict__ rbeg, int64_t* __restrict__ rlen,
                                                         uint8_t* __restrict__ rpiv, int64_t* __restrict__ cbeg,
                                                         int32_t* __restrict__ clen) {
-    const int W = L.width;
     const int nb = L.nb;
+    int32_t buf[kMaxK];
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t* row = F + r * W;
+        const int32_t* row = frontier_row(F, r, buf);
         int64_t lov = -1, hiv = n;
         for (int q = 0; q < L.nlo; ++q) lov = max(lov, (int64_t)row[L.lo[q]]);
         for (int q = 0; q < L.nhi; ++q) hiv = min(hiv, (int64_t)row[L.hi[q]]);
@@ -393,7 +525,7 @@ __global__ void __launch_bounds__(kThreads) k_plan_rows(const int32_t* __restric
     }
 }
 
-void launch_plan_rows(const DevGraph& g, const int32_t* F, int64_t R, const LevelPlan& L, int64_t* rbeg,
+void launch_plan_rows(const DevGraph& g, const Frontier& F, int64_t R, const LevelPlan& L, int64_t* rbeg,
                       int64_t* rlen, uint8_t* rpiv, int64_t* cbeg, int32_t* clen, cudaStream_t s) {
     k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, L.keyed ? g.lkeys : g.cols, g.up, g.n, rbeg, rlen,
                                                  rpiv, cbeg, clen);
@@ -476,8 +608,8 @@ int64_t expand_tile(int width) {
 
 // shared-memory layout of one expand tile (TD merge steps => <= TD+1 rows, <= TD items)
 struct ExpandSmem {
-    size_t P, Beg, CB, Row, CL, RowOf, Piv, Out, total;
-    __host__ __device__ ExpandSmem(int64_t TD, int W, int nb, bool count_only) {
+    size_t P, Beg, CB, Row, CL, RowOf, Piv, LA, Out, total;
+    __host__ __device__ ExpandSmem(int64_t TD, int W, int nb, bool count_only, int nla = 0) {
         const size_t R1 = (size_t)TD + 1;
         P = 0;                     // int64 [R1+1]  work offsets of the tile's rows
         Beg = P + 8 * (R1 + 1);    // int64 [R1]    pivot segment start
@@ -486,7 +618,8 @@ struct ExpandSmem {
         CL = Row + 4 * R1 * W;     // int32 [R1*nb] membership segment length
         RowOf = CL + 4 * R1 * nb;  // int32 [TD]    item -> local row (scatter + max-scan)
         Piv = RowOf + 4 * (size_t)TD;  // uint8 [R1]
-        Out = (Piv + R1 + 15) & ~(size_t)15;
+        LA = Piv + R1;                 // uint8 [R1*2*nla] look-ahead exclusions per row
+        Out = (LA + R1 * 2 * nla + 15) & ~(size_t)15;
         total = Out + (count_only ? 0 : 4 * (size_t)TD * (W + 1));
     }
 };
@@ -517,7 +650,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
     const int64_t TD = a.TD;
     const int W = L.width;
     const int nb = L.nb;
-    const ExpandSmem lay(TD, W, nb, kCountOnly);
+    const ExpandSmem lay(TD, W, nb, kCountOnly, L.nla);
     int64_t* sP = reinterpret_cast<int64_t*>(smem + lay.P);
     int64_t* sBeg = reinterpret_cast<int64_t*>(smem + lay.Beg);
     int64_t* sCB = reinterpret_cast<int64_t*>(smem + lay.CB);
@@ -525,6 +658,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
     int32_t* sCL = reinterpret_cast<int32_t*>(smem + lay.CL);
     int32_t* sRowOf = reinterpret_cast<int32_t*>(smem + lay.RowOf);
     uint8_t* sPiv = smem + lay.Piv;
+    uint8_t* sLA = smem + lay.LA;
     int32_t* sOut = reinterpret_cast<int32_t*>(smem + lay.Out);
     using BlockScan = cub::BlockScan<int, kThreads>;
     __shared__ typename BlockScan::TempStorage scan_tmp;
@@ -558,9 +692,22 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
             sPiv[lr] = a.rpiv[ra0 + lr];
         }
         {
-            const int32_t* src = a.F + ra0 * W;
-            const int nq = nrows * W;
-            for (int q = threadIdx.x; q < nq; q += kThreads) sRow[q] = src[q];
+            if (a.F.rows) {
+                const int32_t* src = a.F.rows + ra0 * W;
+                const int nq = nrows * W;
+                for (int q = threadIdx.x; q < nq; q += kThreads) sRow[q] = src[q];
+            } else {  // compressed frontier: one thread per row walks its (parent, vertex) chain
+                for (int lr = threadIdx.x; lr < nrows; lr += kThreads) {
+                    int64_t r = ra0 + lr;
+                    int32_t* dst = sRow + lr * W;
+                    for (int w = W; w > a.F.bw; --w) {
+                        const int2 e = a.F.pv[w][r];
+                        dst[w - 1] = e.y;
+                        r = e.x;
+                    }
+                    for (int c = 0; c < a.F.bw; ++c) dst[c] = a.F.base[r * a.F.bw + c];
+                }
+            }
             const int nc = nrows * nb;
             for (int q = threadIdx.x; q < nc; q += kThreads) {
                 sCB[q] = a.cbeg[ra0 * nb + q];
@@ -569,6 +716,24 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
         }
         if (threadIdx.x == 0) sCount = 0;
         __syncthreads();
+        if (L.nla) {
+            // look-ahead exclusions of the row: mapped vertices known to be neighbours of the new
+            // image v (the f(j), j in B(i)) that are themselves candidates of target u' (or ok1)
+            const MaskT* __restrict__ ok1 = static_cast<const MaskT*>(a.la_ok1);
+            for (int lr = threadIdx.x; lr < nrows; lr += kThreads) {
+                const int32_t* row = sRow + lr * W;
+                for (int t = 0; t < L.nla; ++t) {
+                    int e1 = 0, e2 = 0;
+                    for (int q = 0; q < nb; ++q) {
+                        const int32_t f = row[L.bpos[q]] & L.idmask;
+                        e1 += (cmask[f] >> L.la_u[t]) & 1u;
+                        if (L.la_depth >= 2) e2 += (ok1[f] >> L.la_u[t]) & 1u;
+                    }
+                    sLA[(lr * L.nla + t) * 2] = (uint8_t)e1;
+                    sLA[(lr * L.nla + t) * 2 + 1] = (uint8_t)e2;
+                }
+            }
+        }
         for (int lr = threadIdx.x; lr < nrows; lr += kThreads) {
             const int64_t s = max(sP[lr], ib0), e = min(sP[lr + 1], ib1);
             if (e > s) sRowOf[s - ib0] = lr;  // rows with items in this tile start at distinct slots
@@ -665,6 +830,17 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
                 for (int j = 0; j < U; ++j)
                     if (act[j]) { ++st_probes; ok[j] = (*pb[j] == (L.key_base | v[j])); }
             }
+            if (L.nla) {  // k-look-ahead: every unmapped query neighbour u' of π[i] keeps a host
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    for (int t = 0; t < L.nla && ok[j]; ++t) {
+                        const int64_t x = (int64_t)v[j] * a.la_k + L.la_u[t];
+                        const uint8_t* ex = sLA + (lr[j] * L.nla + t) * 2;
+                        ok[j] = a.la_c1[x] > ex[0];
+                        if (ok[j] && L.la_depth >= 2) ok[j] = a.la_c2[x] > ex[1];
+                    }
+                }
+            }
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (kCountOnly) {
@@ -676,10 +852,16 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
                     wbase = __shfl_sync(0xffffffffu, wbase, 0);
                     if (ok[j]) {
                         const int pos = wbase + __popc(ball & ((1u << lane) - 1u));
-                        int32_t* o = sOut + (int64_t)pos * (W + 1);
-                        const int32_t* row = sRow + lr[j] * W;
-                        for (int c = 0; c < W; ++c) o[c] = row[c];
-                        o[W] = v[j];
+                        if (a.out_pv) {  // compressed: (input row index, vertex)
+                            int32_t* o = sOut + (int64_t)pos * 2;
+                            o[0] = (int32_t)(ra0 + lr[j]);
+                            o[1] = v[j];
+                        } else {
+                            int32_t* o = sOut + (int64_t)pos * (W + 1);
+                            const int32_t* row = sRow + lr[j] * W;
+                            for (int c = 0; c < W; ++c) o[c] = row[c];
+                            o[W] = v[j];
+                        }
                     }
                 }
             }
@@ -690,8 +872,9 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
             if (threadIdx.x == 0) sBase = total ? atomicAdd(a.out_count, (unsigned long long)total) : 0ull;
             __syncthreads();
             cnt += (threadIdx.x == 0) ? (unsigned long long)total : 0ull;
-            int32_t* dst = a.out + sBase * (W + 1);
-            const int nq = total * (W + 1);
+            const int ow = a.out_pv ? 2 : W + 1;
+            int32_t* dst = a.out_pv ? reinterpret_cast<int32_t*>(a.out_pv) + sBase * 2 : a.out + sBase * (W + 1);
+            const int nq = total * ow;
             for (int q = threadIdx.x; q < nq; q += kThreads) dst[q] = sOut[q];
         }
     }
@@ -832,7 +1015,8 @@ __global__ void __launch_bounds__(kThreads) k_count_walk(ExpandArgs a, LevelPlan
                 ok = (cmask[v] >> L.qv) & 1u;
             }
             if (ok && L.ninj) {
-                const int32_t* row = a.F + r * W;
+                int32_t buf[kMaxK];
+                const int32_t* row = frontier_row(a.F, r, buf);
                 for (int q = 0; q < L.ninj && ok; ++q) ok = v != row[L.inj[q]];
             }
             const int32_t key = L.key_base | v;
@@ -894,7 +1078,7 @@ static int expand_ilp() { return knobs().expand_ilp; }
 
 template <typename MaskT, bool kCountOnly, int U>
 static void launch_expand_u(const ExpandArgs& a, const LevelPlan& L, cudaStream_t s) {
-    const size_t smem = ExpandSmem(a.TD, L.width, L.nb, kCountOnly).total;
+    const size_t smem = ExpandSmem(a.TD, L.width, L.nb, kCountOnly, L.nla).total;
     // per launch: the attribute is per device, and a process may drive several devices
     GSM_CUDA(cudaFuncSetAttribute(k_expand<MaskT, kCountOnly, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
@@ -988,7 +1172,8 @@ __global__ void __launch_bounds__(kThreads) k_tail(TailArgs a, LevelPlan Lc, Lev
             if (lane == 0) a.overflow[atomicAdd(a.noverflow, 1ull)] = r;
             continue;
         }
-        const int32_t* row = a.F + r * W;
+        int32_t rowbuf[kMaxK];
+        const int32_t* row = frontier_row(a.F, r, rowbuf);
         const int piv = a.rpiv[r];
         const int64_t beg = a.rbeg[r];
         if (a.cyc) t_row = clock64();
@@ -1194,7 +1379,8 @@ __global__ void __launch_bounds__(kTBThreads) k_tail_block(TailArgs a, LevelPlan
             if (threadIdx.x == 0) a.overflow[atomicAdd(a.noverflow, 1ull)] = r;
             continue;
         }
-        const int32_t* row = a.F + r * W;
+        int32_t rowbuf[kMaxK];
+        const int32_t* row = frontier_row(a.F, r, rowbuf);
         const int piv = a.rpiv[r];
         const int64_t beg = a.rbeg[r];
         __syncthreads();
@@ -1368,7 +1554,8 @@ __global__ void __launch_bounds__(kThreads) k_pair(PairArgs a, LevelPlan Lp, Lev
         }
         const int64_t ri = cbase++;
         const int64_t r = a.rows_idx ? a.rows_idx[ri] : ri;
-        const int32_t* row = a.F + r * W;
+        int32_t rowbuf[kMaxK];
+        const int32_t* row = frontier_row(a.F, r, rowbuf);
         unsigned long long cp = 0, cq = 0, cb = 0;
         {   // candidates of p
             const int64_t len = a.plen[r], beg = a.pbeg[r];
@@ -1444,7 +1631,8 @@ __global__ void __launch_bounds__(kThreads) k_pair_thread(PairArgs a, LevelPlan 
             a.overflow[atomicAdd(a.noverflow, 1ull)] = r;
             continue;
         }
-        const int32_t* row = a.F + r * W;
+        int32_t rowbuf[kMaxK];
+        const int32_t* row = frontier_row(a.F, r, rowbuf);
         unsigned long long cp = 0, cq = 0, cb = 0;
         const int64_t pb = a.pbeg[r], qb = a.qbeg[r];
         const int ppv = a.ppiv[r], qpv = a.qpiv[r];
@@ -1585,17 +1773,19 @@ void launch_tail(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, in
     }
 }
 
-__global__ void k_gather_overflow(const int32_t* __restrict__ F, int W, const int64_t* __restrict__ idx, int64_t n,
+__global__ void k_gather_overflow(const Frontier F, const int64_t* __restrict__ idx, int64_t n,
                                   int32_t* __restrict__ out) {
-    const int64_t total = n * W;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / W;
-        out[i] = F[idx[r] * W + (i - r * W)];
+    const int W = F.W;
+    int32_t buf[kMaxK];
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t* row = frontier_row(F, idx[r], buf);
+        for (int c = 0; c < W; ++c) out[r * W + c] = row[c];
     }
 }
 
-void launch_gather_rows(const int32_t* F, int W, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s) {
-    k_gather_overflow<<<grid_for(n * W), kThreads, 0, s>>>(F, W, idx, n, out);
+// rows idx[0..n) of F, materialised as plain rows (width F.W)
+void launch_gather_rows(const Frontier& F, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s) {
+    k_gather_overflow<<<grid_for(n), kThreads, 0, s>>>(F, idx, n, out);
     GSM_LAUNCH("k_gather_overflow");
 }
 

@@ -19,6 +19,38 @@ struct FilterQuery {
 // mask width: 1, 2 or 4 bytes per vertex (k <= 8, 16, 32)
 inline int mask_bytes_for(int k) { return k <= 8 ? 1 : (k <= 16 ? 2 : 4); }
 
+// ----------------------------------------------------------------------------
+// A frontier of partial results (Alg. 1's M[i]) of width W, in one of two layouts:
+//  * plain: int32 rows, row-major (4 W bytes per row);
+//  * compressed ("store the value to partial
+//    results ... to further save memory usage", P:163 optimisation 4): level-wise
+//    (parent index, vertex) pairs — row r of width w is row pv[w][r].x of width w-1
+//    extended by vertex pv[w][r].y — 8 bytes per row at any width; the chain ends in a
+//    plain frontier `base` of width bw (the roots, or rows handed over in plain form).
+// Depth-first chunk processing keeps every ancestor chunk resident while its children
+// are expanded, so a chain is always valid.  Bijective (the tuple is recovered exactly,
+// unlike a lossy hash, so listings stay possible — DESIGN.md reading R6).
+// ----------------------------------------------------------------------------
+struct Frontier {
+    int32_t W = 0;
+    const int32_t* rows = nullptr;     // plain rows (width W), or nullptr when compressed
+    const int32_t* base = nullptr;     // compressed: plain rows of width bw the chains end in
+    int32_t bw = 0;
+    const int2* pv[kMaxK + 1] = {};    // compressed: pv[w] for w = bw+1 .. W
+};
+
+// the row as a pointer: into the plain rows, or reconstructed into buf (W <= kMaxK)
+__device__ __forceinline__ const int32_t* frontier_row(const Frontier& F, int64_t r, int32_t* buf) {
+    if (F.rows) return F.rows + r * F.W;
+    for (int w = F.W; w > F.bw; --w) {
+        const int2 e = F.pv[w][r];
+        buf[w - 1] = e.y;
+        r = e.x;
+    }
+    for (int c = 0; c < F.bw; ++c) buf[c] = F.base[r * F.bw + c];
+    return buf;
+}
+
 // K1 (Alg. 1 line 8): cmask[v] bit u = [label(v) = label_Q(u)] and [deg(v) >= deg_Q(u)];
 // counts[u] += |C(u)|  (counts must be zeroed by the caller).
 void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigned long long* counts,
@@ -26,6 +58,9 @@ void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigne
 
 // K5 NE refinement (Alg. 1 lines 7-8): `rounds` passes of NE / effective-degree pruning of
 // cmask (qne: device int64[k] query NE), then counts[u] = |C(u)| recomputed.  tmp: n mask words.
+// out[new2old[v]] = (uint32) cmask[v]
+void launch_mask_to_original(const DevGraph& g, const void* cmask, int mask_bytes, uint32_t* out, cudaStream_t s);
+
 void launch_refine(const DevGraph& g, const FilterQuery& q, const int64_t* qne, int rounds, void* cmask, void* tmp,
                    unsigned long long* counts, cudaStream_t s);
 
@@ -42,7 +77,7 @@ int64_t launch_root_subset(const DevGraph& g, const void* cmask, int mask_bytes,
 // Also writes, per row and per backward position q, the exact admissible segment of that
 // neighbour's list (cbeg/clen, R x nb): the pivot's is the candidate list, the others are
 // the membership lists the verify step binary-searches.
-void launch_plan_rows(const DevGraph& g, const int32_t* F, int64_t R, const LevelPlan& L, int64_t* rbeg,
+void launch_plan_rows(const DevGraph& g, const Frontier& F, int64_t R, const LevelPlan& L, int64_t* rbeg,
                       int64_t* rlen, uint8_t* rpiv, int64_t* cbeg, int32_t* clen, cudaStream_t s);
 
 // Inclusive scan of rlen into P[1..R] (P[0] = 0); returns nothing (caller reads P[R]).
@@ -54,7 +89,7 @@ void launch_partition(const int64_t* P, int64_t R, int64_t S, int64_t D0, int64_
                       int64_t* tile_ra, cudaStream_t s);
 
 struct ExpandArgs {
-    const int32_t* F;      // input rows (R x width)
+    Frontier F;            // input rows (R x width)
     int64_t R;
     const int64_t* P;      // R+1 work offsets
     const int64_t* rbeg;   // R pivot-range starts (index into cols)
@@ -66,10 +101,24 @@ struct ExpandArgs {
     const int64_t* off;
     const int32_t* cols;
     const void* cmask;
-    int32_t* out;          // survivors (width+1 ints each), unless count_only
+    int32_t* out;          // survivors (width+1 ints each), unless count_only or out_pv
+    int2* out_pv;          // compressed output: (input row index, new vertex) per survivor
     unsigned long long* out_count;  // survivors (atomic)
     unsigned long long* stats;      // [items, mask_checked, probes, survivors, lists]
+    // look-ahead tables (L.nla > 0): c1[v*k + u] = min(255, |N(v) ∩ C(u)|); ok1 = per-vertex
+    // mask of u whose later query neighbours all have a candidate neighbour; c2[v*k + u] =
+    // min(255, |{w ∈ N(v) : ok1[w] bit u}|)
+    const uint8_t* la_c1;
+    const uint8_t* la_c2;
+    const void* la_ok1;
+    int32_t la_k;
 };
+
+// look-ahead precomputation (one edge pass each): out[v*k + u] = min(255, |{w in N(v): mask[w] bit u}|)
+void launch_la_counts(const DevGraph& g, int k, int mask_bytes, const void* mask, uint8_t* out, cudaStream_t s);
+// ok1[w] = bits u with cmask[w] bit u and c1[w*k + u''] >= 1 for every u'' in dmask[u]
+void launch_la_ok1(const DevGraph& g, int k, int mask_bytes, const void* cmask, const uint8_t* c1,
+                   const uint32_t* dmask_host, void* ok1, cudaStream_t s);
 
 // Tile size (merge steps per CTA) for a given input width / for a level plan (the COUNT-mode
 // last level uses the walking kernel with its own, larger tile).
@@ -81,7 +130,7 @@ void launch_expand(const ExpandArgs& a, const LevelPlan& L, int mask_bytes, cuda
 
 // Fused tail (COUNT mode): positions k-2 and k-1 in one kernel (candidate-set inheritance).
 struct TailArgs {
-    const int32_t* F;       // rows of width k-2
+    Frontier F;             // rows of width k-2
     int64_t R;
     const int64_t* rbeg;    // plan of position k-2 (k_plan_rows)
     const int64_t* rlen;
@@ -112,12 +161,12 @@ int tail_bratio();
 int tail_block_cap();
 void launch_tail_block(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s);
 void launch_tail(const TailArgs& a, const LevelPlan& Lc, const LevelPlan& Ld, int mask_bytes, cudaStream_t s);
-void launch_gather_rows(const int32_t* F, int W, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s);
+void launch_gather_rows(const Frontier& F, const int64_t* idx, int64_t n, int32_t* out, cudaStream_t s);
 
 // Pair tail (COUNT mode): positions p = k-2 and q = k-1 not adjacent in Q and without an ID
 // condition between them: count(r) = |Cp(r)| |Cq(r)| - |Cp(r) ∩ Cq(r)| per row r of width k-2.
 struct PairArgs {
-    const int32_t* F;
+    Frontier F;
     int64_t R;
     const int64_t *pbeg, *plen, *pcbeg;  // k_plan_rows of position p
     const uint8_t* ppiv;
@@ -156,6 +205,8 @@ struct CliqueRun {
     int32_t* over_roots;    // out (capacity R): roots with |N+(u)| beyond the per-CTA tables,
     int64_t n_over;         // left to the breadth-first path (set by run_clique)
     struct Workspace* ws;   // per-graph grow-only buffers (gsm_workspace.h)
+    const uint32_t* hub_bits = nullptr;  // DevGraph hub bitmap (nullptr = none)
+    int32_t hub_base = 0, hub_words = 0;
 };
 int64_t run_clique(CliqueRun& r, cudaStream_t s);  // returns kernel launches
 int clique_dsmem(int K);

@@ -99,10 +99,16 @@ class Matcher {
     void run();
 
    private:
-    void process(int w, const int32_t* F, int64_t R);
-    void process_generic(int w, const int32_t* F, int64_t R);
-    void process_tail(int w, const int32_t* F, int64_t R);
-    void process_pair(int w, const int32_t* F, int64_t R);
+    void process(int w, const Frontier& F, int64_t R);
+    void process_generic(int w, const Frontier& F, int64_t R);
+    void process_tail(int w, const Frontier& F, int64_t R);
+    void process_pair(int w, const Frontier& F, int64_t R);
+    static Frontier plain(const int32_t* rows, int w) {
+        Frontier f;
+        f.W = w;
+        f.rows = rows;
+        return f;
+    }
     bool tail_eligible(TailArgs* ta) const;
     bool clique_eligible() const;
     void append_output(const int32_t* rows, int64_t R);
@@ -138,6 +144,7 @@ class Matcher {
     bool pair_ = false;        // COUNT: last two positions independent (k_pair)
     LevelPlan lq_;             // plan of position k-1 over rows of width k-2 (pair tail)
     double pair_rows_ = 0;
+    bool compress_ = false;    // intermediate frontiers as (parent, vertex) pairs
 };
 
 void Matcher::run() {
@@ -219,6 +226,46 @@ void Matcher::run() {
         }
     }
 
+    // ---- k-look-ahead: per position, the unmapped query neighbours of π[i]
+    {
+        const int la = knobs().lookahead >= 0 ? knobs().lookahead : opts_.lookahead;
+        bool any = false;
+        for (int i = 1; i < k_; ++i) {
+            LevelPlan& L = lplan_[i];
+            L.nla = 0;
+            L.la_depth = la;
+            if (la <= 0) continue;
+            for (int p = i + 1; p < k_; ++p) {
+                const int u = plan_.order[p];
+                if ((plan_.adj[plan_.order[i]] >> u) & 1u) L.la_u[L.nla++] = u;
+            }
+            any |= L.nla > 0;
+        }
+        if (any && !empty) {
+            ws_.la_c1.ensure((size_t)g_.n * k_, s_);
+            rec_.run(GSM_K_FILTER, 1, [&] { launch_la_counts(g_, k_, mask_bytes_, cmask_.p, ws_.la_c1.p, s_); });
+            res_->prof[GSM_K_FILTER].alg_bytes += (double)g_.nnz * (4.0 + mask_bytes_) + (double)g_.n * (16.0 + k_);
+            if (la >= 2) {
+                // D(u) = query neighbours of u placed after u; ok1[w] bit u = w hosts u and has a
+                // candidate neighbour for every vertex of D(u)
+                uint32_t dmask[kMaxK] = {};
+                for (int u = 0; u < k_; ++u)
+                    for (int w = 0; w < k_; ++w)
+                        if (((plan_.adj[u] >> w) & 1u) && plan_.pos[w] > plan_.pos[u]) dmask[u] |= 1u << w;
+                ws_.la_ok1.ensure((size_t)g_.n * mask_bytes_, s_);
+                ws_.la_c2.ensure((size_t)g_.n * k_, s_);
+                rec_.run(GSM_K_FILTER, 2, [&] {
+                    launch_la_ok1(g_, k_, mask_bytes_, cmask_.p, ws_.la_c1.p, dmask, ws_.la_ok1.p, s_);
+                    launch_la_counts(g_, k_, mask_bytes_, ws_.la_ok1.p, ws_.la_c2.p, s_);
+                });
+                res_->prof[GSM_K_FILTER].alg_bytes += (double)g_.n * (2.0 * mask_bytes_ + k_) +
+                                                      (double)g_.nnz * (4.0 + mask_bytes_) + (double)g_.n * (16.0 + k_);
+            }
+        } else {
+            for (int i = 1; i < k_; ++i) lplan_[i].nla = 0;
+        }
+    }
+
     tail_ = tail_eligible(&tail_args_);
     clique_ = clique_eligible();
     if (pair_) {
@@ -256,6 +303,7 @@ void Matcher::run() {
         res_->prof[GSM_K_ROOTS].alg_bytes += 2.0 * (double)g_.n * mask_bytes_ + 4.0 * (double)R0;
     }
     res_->level_rows[0] = (uint64_t)R0;
+    res_->level_frontier_bytes[0] = 4 * (uint64_t)R0;
     res_->ms_filter = (float)ms_since(t0);
 
     // ---- verify iterations (Alg. 1 lines 10-15)
@@ -284,11 +332,14 @@ void Matcher::run() {
         budget_ = opts_.mem_budget_bytes ? (int64_t)opts_.mem_budget_bytes
                                          : (int64_t)std::min((double)total_b / 4.0, avail);
     }
+    compress_ = ((opts_.flags & GSM_FLAG_COMPRESSED_PARTIALS) || knobs().compress > 0) && knobs().compress != 0;
+    res_->compressed = compress_ ? 1 : 0;
     // per-width share of the budget for frontiers of width 2..k (k only when enumerating)
     const int nfront = count_mode_ ? std::max(0, k_ - 2) : k_ - 1;
     for (int w = 2; w <= k_; ++w) {
         const int64_t share = nfront > 0 ? budget_ / nfront : budget_;
-        const int64_t per_row = 4 * w + 8 * 3 + 1 + 1 + 12 * (w - 1);  // rows + rbeg/rlen/P + piv + segs
+        // stored partial result + its row plan (rbeg/rlen/P, piv, per-backward segments)
+        const int64_t per_row = (compress_ && w < k_ ? 8 : 4 * w) + 8 * 3 + 1 + 1 + 12 * (w - 1);
         lv_[w]->cap_rows = std::max<int64_t>(share / per_row, 1);
     }
 
@@ -310,15 +361,18 @@ void Matcher::run() {
         over.ensure(R0, s_);
         cr.over_roots = over.p;
         cr.ws = &ws_;
+        cr.hub_bits = g_.hub_bits;
+        cr.hub_base = g_.hub_base;
+        cr.hub_words = g_.hub_words;
         int64_t launches = 0;
         rec_.run(GSM_K_CLIQUE, 1, [&] { launches = run_clique(cr, s_); });
         res_->kernel_launches += launches > 0 ? launches - 1 : 0;
         res_->num_chunks++;
         // roots whose N+(u) exceeds the per-CTA tables: the breadth-first path (same counter)
-        if (cr.n_over > 0) process(1, over.p, cr.n_over);
+        if (cr.n_over > 0) process(1, plain(over.p, 1), cr.n_over);
         found = read_scalar(final_count_.p, s_);
     } else if (R0 > 0) {
-        process(1, lv_[1]->rows.p, R0);
+        process(1, plain(lv_[1]->rows.p, 1), R0);
         if (count_mode_) found = read_scalar(final_count_.p, s_);
         else found = (uint64_t)arena_rows_;
     }
@@ -378,7 +432,7 @@ void Matcher::run() {
     res_->ms_total = (float)ms_since(t_all);
 }
 
-void Matcher::process(int w, const int32_t* F, int64_t R) {
+void Matcher::process(int w, const Frontier& F, int64_t R) {
     if (R <= 0) return;
     if (pair_ && w == k_ - 2) process_pair(w, F, R);
     else if (tail_ && w == k_ - 2) process_tail(w, F, R);
@@ -427,7 +481,7 @@ bool Matcher::tail_eligible(TailArgs* ta) const {
     return true;
 }
 
-void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
+void Matcher::process_tail(int w, const Frontier& F, int64_t R) {
     LevelBufs& B = *lv_[w];
     const LevelPlan& L = lplan_[w];
     B.rbeg.ensure(R, s_);
@@ -497,17 +551,17 @@ void Matcher::process_tail(int w, const int32_t* F, int64_t R) {
     }
     if (nov > 0) {  // still too big for a CTA: generic breadth-first path
         ovf_rows_.ensure((size_t)nov * w, s_);
-        launch_gather_rows(F, w, ovf_idx_.p, nov, ovf_rows_.p, s_);
+        launch_gather_rows(F, ovf_idx_.p, nov, ovf_rows_.p, s_);
         res_->kernel_launches++;
         DevBuf<int32_t> rows;
         rows.ensure((size_t)nov * w, s_);
         GSM_CUDA(cudaMemcpyAsync(rows.p, ovf_rows_.p, sizeof(int32_t) * nov * w, cudaMemcpyDeviceToDevice, s_));
-        process_generic(w, rows.p, nov);
+        process_generic(w, plain(rows.p, w), nov);
     }
 }
 
 // Pair tail (COUNT): per row of width k-2, |Cp| |Cq| - |Cp ∩ Cq| (k_pair)
-void Matcher::process_pair(int w, const int32_t* F, int64_t R) {
+void Matcher::process_pair(int w, const Frontier& F, int64_t R) {
     LevelBufs& B = *lv_[w];
     const LevelPlan& Lp = lplan_[w];
     B.rbeg.ensure(R, s_);
@@ -576,7 +630,7 @@ void Matcher::process_pair(int w, const int32_t* F, int64_t R) {
     pair_rows_ += (double)R;
 }
 
-void Matcher::process_generic(int w, const int32_t* F, int64_t R) {
+void Matcher::process_generic(int w, const Frontier& F, int64_t R) {
     if (R <= 0) return;
     LevelBufs& B = *lv_[w];
     const LevelPlan& L = lplan_[w];
@@ -600,6 +654,8 @@ void Matcher::process_generic(int w, const int32_t* F, int64_t R) {
     const int64_t TD = expand_tile_for(L);
     const bool last = (w == k_ - 1);
     int64_t chunk;
+    // intermediate output (not the last level) in the compressed layout when enabled
+    const bool cout = compress_ && !last;
     if (last && count_mode_) {
         chunk = TD * ((int64_t)1 << 22);  // only bounds the tile array
     } else {
@@ -607,7 +663,8 @@ void Matcher::process_generic(int w, const int32_t* F, int64_t R) {
         if (chunk < TD) chunk = std::min<int64_t>(total, TD);
         for (;;) {  // the budget is an estimate: on OOM halve this level's chunk (down to one tile)
             try {
-                lv_[w + 1]->rows.ensure((size_t)chunk * (w + 1), s_);
+                if (cout) lv_[w + 1]->pv.ensure((size_t)chunk, s_);
+                else lv_[w + 1]->rows.ensure((size_t)chunk * (w + 1), s_);
                 break;
             } catch (const Failure& f) {
                 if (f.status != GSM_ERR_OUT_OF_MEMORY || chunk <= TD) throw;
@@ -635,6 +692,10 @@ void Matcher::process_generic(int w, const int32_t* F, int64_t R) {
     a.cols = L.keyed ? g_.lkeys : g_.cols;
     a.cmask = cmask_.p;
     a.stats = B.stats;
+    a.la_c1 = ws_.la_c1.p;
+    a.la_c2 = ws_.la_c2.p;
+    a.la_ok1 = ws_.la_ok1.p;
+    a.la_k = k_;
     B.rows_in += (double)R;
     for (int64_t D0 = 0; D0 < total; D0 += chunk) {
         const int64_t D1 = std::min(D0 + chunk, total);
@@ -653,13 +714,28 @@ void Matcher::process_generic(int w, const int32_t* F, int64_t R) {
         }
         LevelBufs& N = *lv_[w + 1];
         GSM_CUDA(cudaMemsetAsync(N.out_count.p, 0, sizeof(unsigned long long), s_));
-        a.out = N.rows.p;
+        a.out = cout ? nullptr : N.rows.p;
+        a.out_pv = cout ? N.pv.p : nullptr;
         a.out_count = N.out_count.p;
         rec_.run(GSM_K_EXPAND, 1, [&] { launch_expand(a, L, mask_bytes_, s_); });
         const int64_t R2 = (int64_t)read_scalar(N.out_count.p, s_);
         if (R2 == 0) continue;
-        if (last) append_output(N.rows.p, R2);
-        else process(w + 1, N.rows.p, R2);
+        res_->level_frontier_bytes[w] += (uint64_t)R2 * (cout ? 8u : 4u * (w + 1));
+        if (last) {
+            append_output(N.rows.p, R2);
+        } else if (cout) {  // the new level extends F's chains by (row of F, vertex) pairs
+            Frontier F2 = F;
+            if (F.rows) {
+                F2.rows = nullptr;
+                F2.base = F.rows;
+                F2.bw = F.W;
+            }
+            F2.W = w + 1;
+            F2.pv[w + 1] = N.pv.p;
+            process(w + 1, F2, R2);
+        } else {
+            process(w + 1, plain(N.rows.p, w + 1), R2);
+        }
     }
 }
 
@@ -738,6 +814,7 @@ void match_impl(const gsm_graph* gh, const gsm_query* q, const gsm_match_opts* u
     if (opts.num_shards > 1 && (opts.shard_index < 0 || opts.shard_index >= opts.num_shards))
         fail(GSM_ERR_INVALID_ARGUMENT, "shard_index out of range");
     if (opts.refine_rounds < 0 || opts.refine_rounds > 64) fail(GSM_ERR_INVALID_ARGUMENT, "refine_rounds out of range");
+    if (opts.lookahead < 0 || opts.lookahead > 2) fail(GSM_ERR_INVALID_ARGUMENT, "lookahead must be 0, 1 or 2");
     if (opts.root_subset_len < 0 || (opts.root_subset_len > 0 && !opts.root_subset))
         fail(GSM_ERR_INVALID_ARGUMENT, "bad root_subset");
     if (!opts.root_subset) opts.root_subset_len = 0;
@@ -880,6 +957,74 @@ gsm_status gsm_sort_rows(int32_t* rows, uint64_t num_rows, int32_t width, int64_
     } catch (...) {
         cudaSetDevice(prev);
         gsm::set_error("unexpected exception in gsm_sort_rows");
+        return GSM_ERR_CUDA;
+    }
+}
+
+gsm_status gsm_filter_candidates(const gsm_graph* g, const gsm_query* q, int32_t refine_rounds, uint32_t* out,
+                                 int32_t out_on_device) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    try {
+        gsm::clear_error();
+        gsm::load_knobs();
+        if (!g || !out) gsm::fail(GSM_ERR_INVALID_ARGUMENT, "graph or out is NULL");
+        if (refine_rounds < 0 || refine_rounds > 64) gsm::fail(GSM_ERR_INVALID_ARGUMENT, "refine_rounds out of range");
+        gsm::QueryPlan plan;
+        std::string msg;
+        gsm_status st = gsm::load_query(q, &plan, &msg);
+        if (st != GSM_OK) gsm::fail(st, msg);
+        if (plan.use_labels && !gsm::labeled_of(g))
+            gsm::fail(GSM_ERR_INVALID_ARGUMENT, "query has labels but the data graph is unlabeled");
+        GSM_CUDA(cudaSetDevice(gsm::device_of(g)));
+        const gsm::DevGraph& G = gsm::graph_of(g);
+        cudaStream_t s = gsm::stream_of(g);
+        const int k = plan.k, mb = gsm::mask_bytes_for(k);
+        gsm::FilterQuery fq;
+        std::memset(&fq, 0, sizeof(fq));
+        fq.k = k;
+        fq.use_labels = plan.use_labels ? 1 : 0;
+        for (int u = 0; u < k; ++u) {
+            fq.qlabel[u] = plan.qlabel[u];
+            fq.qdeg[u] = plan.qdeg[u];
+            fq.qadj[u] = plan.adj[u];
+        }
+        gsm::Workspace& ws = gsm::workspace_of(g);
+        ws.cmask.ensure((size_t)G.n * mb, s);
+        ws.counts.ensure(gsm::kMaxK, s);
+        GSM_CUDA(cudaMemsetAsync(ws.counts.p, 0, sizeof(unsigned long long) * gsm::kMaxK, s));
+        gsm::launch_filter(G, fq, ws.cmask.p, ws.counts.p, s);
+        if (refine_rounds > 0) {
+            int64_t hqne[gsm::kMaxK] = {};
+            for (int u = 0; u < k; ++u)
+                for (int w = 0; w < k; ++w)
+                    if ((plan.adj[u] >> w) & 1u) hqne[u] += plan.use_labels ? (int64_t)plan.qlabel[w] + 1 : 1;
+            gsm::DevBuf<int64_t> dqne;
+            gsm::DevBuf<uint8_t> tmp;
+            dqne.ensure(gsm::kMaxK, s);
+            tmp.ensure((size_t)G.n * mb, s);
+            GSM_CUDA(cudaMemcpyAsync(dqne.p, hqne, sizeof(hqne), cudaMemcpyHostToDevice, s));
+            gsm::launch_refine(G, fq, dqne.p, refine_rounds, ws.cmask.p, tmp.p, ws.counts.p, s);
+        }
+        gsm::DevBuf<uint32_t> dout;
+        uint32_t* dst = out;
+        if (!out_on_device) {
+            dout.ensure((size_t)G.n, s);
+            dst = dout.p;
+        }
+        gsm::launch_mask_to_original(G, ws.cmask.p, mb, dst, s);
+        if (!out_on_device)
+            GSM_CUDA(cudaMemcpyAsync(out, dout.p, sizeof(uint32_t) * G.n, cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        cudaSetDevice(prev);
+        return GSM_OK;
+    } catch (const gsm::Failure& f) {
+        cudaSetDevice(prev);
+        gsm::set_error(f.msg);
+        return f.status;
+    } catch (...) {
+        cudaSetDevice(prev);
+        gsm::set_error("unexpected exception in gsm_filter_candidates");
         return GSM_ERR_CUDA;
     }
 }

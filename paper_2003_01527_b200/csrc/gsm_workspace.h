@@ -11,7 +11,8 @@
 namespace gsm {
 
 struct LevelBufs {
-    DevBuf<int32_t> rows;  // frontier of this width (input rows of process(width))
+    DevBuf<int32_t> rows;  // frontier of this width (input rows of process(width)), plain layout
+    DevBuf<int2> pv;       // the same frontier in the compressed layout: (parent row, vertex)
     int64_t cap_rows = 0;  // row capacity reserved for this frontier (per match)
     DevBuf<int64_t> rbeg, rlen, P, tile_ra, cbeg;
     DevBuf<int32_t> clen;
@@ -26,6 +27,7 @@ struct Workspace {
     DevBuf<uint8_t> cmask;
     DevBuf<unsigned long long> counts, final_count, stats, ovf_n, sched;
     DevBuf<int64_t> ovf_idx;
+    DevBuf<uint8_t> la_c1, la_c2, la_ok1;  // k-look-ahead tables (gsm_match_opts.lookahead)
     DevBuf<int32_t> ovf_rows;
     // clique path (gsm_clique.cu): root keys / order, sort temp, global slab, handed-back roots
     DevBuf<int32_t> ck_keys, ck_vals, ck_keys2, ck_vals2, ck_slab, ck_over;

@@ -28,6 +28,7 @@ GSM_FLAG_UNIQUE = 1
 GSM_FLAG_NO_SYMMETRY = 2
 GSM_FLAG_PROFILE = 4
 GSM_FLAG_PLAN_COUNT = 8
+GSM_FLAG_COMPRESSED_PARTIALS = 16
 KERNEL_NAMES = ["filter", "roots", "plan", "scan", "expand", "finalize", "tail", "clique"]
 
 
@@ -50,7 +51,7 @@ class gsm_query(ctypes.Structure):
 class gsm_match_opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("mode", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("shard_index", ctypes.c_int32), ("num_shards", ctypes.c_int32), ("refine_rounds", ctypes.c_int32),
-                ("root_subset", ctypes.POINTER(ctypes.c_int32)), ("root_subset_len", ctypes.c_int64),
+                ("lookahead", ctypes.c_int32), ("root_subset", ctypes.POINTER(ctypes.c_int32)), ("root_subset_len", ctypes.c_int64),
                 ("mem_budget_bytes", ctypes.c_uint64), ("stream", ctypes.c_void_p)]
 
 
@@ -67,7 +68,8 @@ class gsm_result(ctypes.Structure):
                 ("order", ctypes.c_int32 * MAX_K), ("candidates", ctypes.c_uint64 * MAX_K),
                 ("level_rows", ctypes.c_uint64 * MAX_K), ("level_work", ctypes.c_uint64 * MAX_K),
                 ("num_chunks", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
-                ("prof", gsm_kernel_prof * 8), ("device", ctypes.c_int32), ("symmetric", ctypes.c_int32)]
+                ("prof", gsm_kernel_prof * 8), ("device", ctypes.c_int32), ("symmetric", ctypes.c_int32),
+                ("level_frontier_bytes", ctypes.c_uint64 * MAX_K), ("compressed", ctypes.c_int32)]
 
 
 class gsm_plan_info(ctypes.Structure):
@@ -80,7 +82,7 @@ class gsm_plan_info(ctypes.Structure):
 _lib = None
 
 EXPORTS = ["gsm_load_graph", "gsm_free", "gsm_graph_info", "gsm_match", "gsm_result_free", "gsm_result_copy_rows",
-           "gsm_plan_query", "gsm_sort_rows", "gsm_last_error", "gsm_version"]
+           "gsm_plan_query", "gsm_sort_rows", "gsm_filter_candidates", "gsm_last_error", "gsm_version"]
 
 
 def lib():
@@ -100,6 +102,7 @@ def lib():
         L.gsm_result_copy_rows.argtypes = [ctypes.POINTER(gsm_result), P, i32]
         L.gsm_plan_query.argtypes = [ctypes.POINTER(gsm_query), P, ctypes.c_uint32, ctypes.POINTER(gsm_plan_info)]
         L.gsm_sort_rows.argtypes = [P, ctypes.c_uint64, i32, i64, i32, P]
+        L.gsm_filter_candidates.argtypes = [P, ctypes.POINTER(gsm_query), i32, P, i32]
         L.gsm_last_error.restype = ctypes.c_char_p
         L.gsm_version.restype = ctypes.c_char_p
         for name in EXPORTS:
@@ -216,6 +219,8 @@ class Result:
         self.order = list(r.order[:k])
         self.candidates = [int(x) for x in r.candidates[:k]]
         self.level_rows = [int(x) for x in r.level_rows[:k]]
+        self.level_frontier_bytes = [int(x) for x in r.level_frontier_bytes[:k]]
+        self.compressed = bool(r.compressed)
         self.level_work = [int(x) for x in r.level_work[:k]]
         self.num_chunks = int(r.num_chunks)
         self.kernel_launches = int(r.kernel_launches)
@@ -251,12 +256,12 @@ class Result:
 
 def gsm_match(g: Graph, num_nodes: int, edges: Sequence, labels=None, mode: int = GSM_MODE_COUNT, flags: int = 0,
               shard_index: int = 0, num_shards: int = 1, root_subset=None, mem_budget_bytes: int = 0,
-              stream: Optional[int] = None, refine_rounds: int = 0) -> Result:
+              stream: Optional[int] = None, refine_rounds: int = 0, lookahead: int = 0) -> Result:
     """Count (mode=GSM_MODE_COUNT) or enumerate (GSM_MODE_ENUMERATE) the embeddings of the
     query (num_nodes, edges, labels) in g.  Rows are freed with gsm_result_free / Result.free."""
     q, keep = _query(num_nodes, edges, labels)
     rs = None if root_subset is None else np.ascontiguousarray(np.asarray(root_subset, dtype=np.int32))
-    opts = gsm_match_opts(ctypes.sizeof(gsm_match_opts), mode, flags, shard_index, num_shards, refine_rounds,
+    opts = gsm_match_opts(ctypes.sizeof(gsm_match_opts), mode, flags, shard_index, num_shards, refine_rounds, lookahead,
                           None if rs is None else rs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                           0 if rs is None else len(rs), mem_budget_bytes, stream)
     r = gsm_result()
@@ -283,6 +288,17 @@ def gsm_sort_rows(rows, max_id: int, stream: Optional[int] = None):
     _check(lib().gsm_sort_rows(ctypes.c_void_p(rows.data_ptr()), rows.shape[0], rows.shape[1], int(max_id),
                                rows.device.index or 0, stream))
     return rows
+
+
+def gsm_filter_candidates(g: Graph, num_nodes: int, edges: Sequence, labels=None, refine_rounds: int = 0):
+    """Candidate masks of the filter step (Alg. 1 lines 6-9): uint32 array, entry v (original
+    id) has bit u set iff v is a candidate of query vertex u."""
+    q, keep = _query(num_nodes, edges, labels)
+    n = gsm_graph_info(g)["num_nodes"]
+    out = np.zeros(n, dtype=np.uint32)
+    _check(lib().gsm_filter_candidates(g.handle, ctypes.byref(q), int(refine_rounds), ctypes.c_void_p(out.ctypes.data), 0))
+    del keep
+    return out
 
 
 def gsm_plan_query(num_nodes: int, edges: Sequence, labels=None, candidates=None, flags: int = 0) -> dict:

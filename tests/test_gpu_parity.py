@@ -151,18 +151,27 @@ def dense_gnp():
     return g, oracle.count_triangles(g), oracle.count_k4(g)
 
 
-@pytest.mark.parametrize("variant", ["default", "warp0", "dsmem64", "search", "stream", "nohash", "handback", "off"])
+@pytest.mark.parametrize("variant", ["default", "nohub", "hubmix", "hubmix_warp0", "warp0", "dsmem64", "search",
+                                     "stream", "nohash", "handback", "off"])
 def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
     """K3/K4 COUNT through the per-root local-bitmap kernels (gsm_clique.cu) in every
     bucket (warp per root; CTA with shared memory; CTA with a global slab via a tiny
     GSM_CLIQUE_DSMEM) and both row-construction strategies, against the oracle (DFS on an
     R-MAT graph, independent clique counters on a dense G(n, p)).  "off" = the fused-tail
     path (GSM_CLIQUE=0) on the same inputs; "handback" = roots beyond GSM_CLIQUE_DMAX handed
-    back to the breadth-first path inside the same call."""
-    env = {"warp0": {"GSM_CLIQUE_WARP": "0"}, "dsmem64": {"GSM_CLIQUE_DSMEM": "64"},
+    back to the breadth-first path inside the same call.  Hub bitmap (read at load time):
+    "default" = every vertex of these small graphs is a hub, so every row is built by
+    bitmap lookups; "hubmix" = only the top 256 ranks are hubs (lookup, stream and search
+    rows mixed in one root); every other variant switches the bitmap off (GSM_HUB_BITS=0)
+    so its stream / search / bucket path is the one under test."""
+    env = {"nohub": {}, "hubmix": {"GSM_HUB_BITS": "256"},
+           "hubmix_warp0": {"GSM_HUB_BITS": "256", "GSM_CLIQUE_WARP": "0", "GSM_CLIQUE_DSMEM": "64"},
+           "warp0": {"GSM_CLIQUE_WARP": "0"}, "dsmem64": {"GSM_CLIQUE_DSMEM": "64"},
            "search": {"GSM_CLIQUE_STREAM": "0"}, "stream": {"GSM_CLIQUE_STREAM": "1000000000"},
            "nohash": {"GSM_CLIQUE_HASH": "0"}, "handback": {"GSM_CLIQUE_DMAX": "64"},
            "off": {"GSM_CLIQUE": "0"}}.get(variant, {})
+    if variant not in ("default", "hubmix", "hubmix_warp0"):
+        env = {"GSM_HUB_BITS": "0", **env}
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = gi.rmat(10, 16, seed=12)
@@ -218,6 +227,61 @@ def test_pair_tail(pair, monkeypatch):
         assert (used > 0) == (pair != "0"), used
     finally:
         G.free()
+
+
+def test_lookahead_results_unchanged():
+    """k-look-ahead: a necessary condition, so the sorted
+    row lists and counts are identical for lookahead = 0, 1, 2 (SPEC criterion 4) on
+    random labeled / unlabeled instances and named queries, in every mode."""
+    n_inst = 0
+    for seed in range(1, 16):
+        g0 = gi.random_gnp(40, 1, 6, 300 + seed)
+        for nl in (0, 3):
+            g = g0.with_labels(gi.uniform_labels(40, 3, seed)) if nl else g0
+            G = load(g)
+            try:
+                for j in range(2):
+                    q = gi.random_connected_query(4 + (seed + j) % 3, (seed + j) % 3, seed * 31 + j, nl)
+                    cnt, ref = oracle.match(g, q)
+                    for la in (1, 2):
+                        c, rows, _ = run(G, q, "enumerate", lookahead=la)
+                        assert c == cnt, (q.name, la)
+                        assert_rows_equal(rows, ref, f"{q.name} la={la}")
+                        for flags in (0, gsm.GSM_FLAG_UNIQUE, gsm.GSM_FLAG_NO_SYMMETRY):
+                            cc, _, r = run(G, q, "count", flags=flags, lookahead=la)
+                            want = cnt if flags != gsm.GSM_FLAG_UNIQUE else cnt // r.automorphisms
+                            assert cc == want, (q.name, la, flags)
+                    n_inst += 1
+            finally:
+                G.free()
+    assert n_inst >= 60
+
+
+def test_lookahead_prunes_on_road_like_graph():
+    """SPEC criterion 4: summed intermediate rows satisfy rows(2) <= rows(1) <= rows(0)
+    on every instance, strictly on the sparse chain-with-tails graph (road_central's low
+    average degree, where Table 2 shows the largest look-ahead gain)."""
+    graphs = [gi.chain_with_tails(400, 6, seed=3), gi.grid(40, 40, seed=5), gi.rmat(10, 4, seed=8)]
+    queries = [gi.query("P4"), gi.query("tailed_triangle"), gi.query("S3"), gi.query("C4"), gi.query("house"),
+               gi.Query(5, [(0, 1), (1, 2), (2, 3), (3, 4)], None, "P5"),
+               gi.Query(5, [(0, 1), (1, 2), (2, 3), (1, 4)], None, "chair")]
+    strict = {}
+    for gi_, g in enumerate(graphs):
+        G = load(g)
+        try:
+            for q in queries:
+                cnt, _ = oracle.match(g, q, count_only=True)
+                rows = []
+                for la in (0, 1, 2):
+                    c, _, r = run(G, q, "enumerate", lookahead=la)
+                    r_rows = sum(r.level_rows[1:q.num_nodes - 1])
+                    assert c == cnt, (g.name, q.name, la)
+                    rows.append(r_rows)
+                assert rows[2] <= rows[1] <= rows[0], (g.name, q.name, rows)
+                strict[(gi_, q.name)] = rows[1] < rows[0] or rows[2] < rows[1]
+        finally:
+            G.free()
+    assert any(v for (gi_, _), v in strict.items() if gi_ == 0), strict
 
 
 def test_ne_refinement_is_sound():
@@ -309,6 +373,84 @@ def test_candidate_counts_match_cpu_predicate():
                 assert r.candidates[u] == int(np.sum(lab_ok & (deg >= qdeg[u]))), (qname, u)
     finally:
         G.free()
+
+
+@pytest.mark.parametrize("variant", ["plain_budget", "budget", "tailcap", "pair_warp"])
+def test_compressed_partials(variant, monkeypatch):
+    """Compressed partial results (level-wise (parent row, vertex) pairs; PAPER P:136/P:151,
+    SURVEY §8(f) row 3): sorted row lists and counts identical to the oracle in every mode,
+    under tiny budgets (chains across many chunks), with the fused tail's overflow hand-back
+    and the pair tail's warp pass reading compressed rows; and the stored bytes of every
+    intermediate width w >= 3 shrink from 4w to 8 per partial result."""
+    if variant == "tailcap":
+        monkeypatch.setenv("GSM_TAIL_CAP", "64")
+        monkeypatch.setenv("GSM_TAIL_BLOCK_CAP", "256")
+    if variant == "pair_warp":
+        monkeypatch.setenv("GSM_PAIR_THREAD_MAX", "0")
+    budget = 0 if variant == "plain_budget" else 1 << 16
+    g = gi.rmat(9, 8, seed=31).with_labels(gi.uniform_labels(512, 2, 31))
+    G = load(g)
+    try:
+        qs = [gi.query("house"), gi.query("K4"), gi.query("P4", [0, 1, 1, 0]), gi.query("C5"),
+              gi.Query(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (0, 3)], None, "C6+chord"),
+              gi.random_connected_query(6, 2, 77, 2)]
+        for q in qs:
+            cnt, ref = oracle.match(g, q)
+            c0, rows0, r0 = run(G, q, "enumerate", mem_budget_bytes=budget)
+            c1, rows1, r1 = run(G, q, "enumerate", flags=gsm.GSM_FLAG_COMPRESSED_PARTIALS, mem_budget_bytes=budget)
+            assert r1.compressed and not r0.compressed
+            assert c0 == c1 == cnt, (variant, q.name)
+            assert_rows_equal(rows1, ref, f"{q.name} compressed")
+            for flags in (0, gsm.GSM_FLAG_UNIQUE, gsm.GSM_FLAG_NO_SYMMETRY):
+                cc, _, r = run(G, q, "count", flags=flags | gsm.GSM_FLAG_COMPRESSED_PARTIALS,
+                               mem_budget_bytes=budget)
+                want = cnt if flags != gsm.GSM_FLAG_UNIQUE else cnt // r.automorphisms
+                assert cc == want, (variant, q.name, flags)
+            k = q.num_nodes
+            for w in range(2, k - 1):  # stored intermediate widths w+1 = 3 .. k-1
+                assert r0.level_rows[w] == r1.level_rows[w]
+                assert r0.level_frontier_bytes[w] == 4 * (w + 1) * r0.level_rows[w]
+                assert r1.level_frontier_bytes[w] == 8 * r1.level_rows[w]
+    finally:
+        G.free()
+
+
+def test_filter_masks_bit_exact():
+    """K1 (vectorised filter): the candidate mask of EVERY vertex equals the CPU predicate
+    label(v) = label_Q(u) and deg(v) >= deg_Q(u) bit for bit — on labeled and
+    unlabeled graphs whose vertex counts are not multiples of 4 (the scalar tail) — and the
+    refined masks are subsets that keep every vertex some oracle embedding uses (soundness)."""
+    cases = [(gi.rmat(12, 8, seed=9).with_labels(gi.uniform_labels(4096, 4, 9)), [("S3", [0, 1, 2, 3]),
+              ("house", [1, 1, 2, 3, 0]), ("K4", None)]),
+             (gi.erdos_renyi(1003, 4000, 2), [("K3", None), ("P4", None), ("C5", None)]),
+             (gi.random_gnp(37, 1, 4, 5).with_labels(gi.uniform_labels(37, 3, 5)), [("tailed_triangle", [0, 1, 2, 0])])]
+    for g, qs in cases:
+        deg = np.diff(g.offsets)
+        G = load(g)
+        try:
+            for qname, ql in qs:
+                q = gi.query(qname, ql)
+                qdeg = np.zeros(q.num_nodes, int)
+                for a, b in q.edges:
+                    qdeg[a] += 1
+                    qdeg[b] += 1
+                want = np.zeros(g.num_nodes, np.uint32)
+                for u in range(q.num_nodes):
+                    lab_ok = np.ones(g.num_nodes, bool) if ql is None else (g.labels == ql[u])
+                    want |= ((lab_ok & (deg >= qdeg[u])).astype(np.uint32) << np.uint32(u))
+                got = gsm.gsm_filter_candidates(G, q.num_nodes, q.edges, q.labels)
+                np.testing.assert_array_equal(got, want, err_msg=qname)
+                _, _, r = run(G, q)
+                for u in range(q.num_nodes):
+                    assert r.candidates[u] == int(np.sum((want >> np.uint32(u)) & 1)), (qname, u)
+                _, ref = oracle.match(g, q)
+                for R in (1, 2):
+                    ref_mask = gsm.gsm_filter_candidates(G, q.num_nodes, q.edges, q.labels, refine_rounds=R)
+                    assert np.all((ref_mask & ~want) == 0), (qname, R)
+                    for u in range(q.num_nodes):
+                        assert np.all((ref_mask[ref[:, u]] >> np.uint32(u)) & 1), (qname, R, u)
+        finally:
+            G.free()
 
 
 def test_chunking_invariance():

@@ -100,6 +100,7 @@ class Matcher {
 
    private:
     void process(int w, const Frontier& F, int64_t R);
+    void ensure_caps();
     void process_generic(int w, const Frontier& F, int64_t R);
     void process_tail(int w, const Frontier& F, int64_t R);
     void process_pair(int w, const Frontier& F, int64_t R);
@@ -145,6 +146,8 @@ class Matcher {
     LevelPlan lq_;             // plan of position k-1 over rows of width k-2 (pair tail)
     double pair_rows_ = 0;
     bool compress_ = false;    // intermediate frontiers as (parent, vertex) pairs
+    bool deferred_counts_ = false;
+    bool caps_ready_ = false;  // |C(u)| read back with the result (unlabeled queries)
 };
 
 void Matcher::run() {
@@ -187,15 +190,27 @@ void Matcher::run() {
             opts_.refine_rounds * ((double)g_.nnz * (4.0 + mask_bytes_ + (plan_.use_labels ? 4.0 : 0.0)) +
                                    (double)g_.n * (16.0 + 3.0 * mask_bytes_)) + (double)g_.n * mask_bytes_;
     }
-    unsigned long long hc[kMaxK];
-    GSM_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, s_));
-    GSM_CUDA(cudaStreamSynchronize(s_));
     uint64_t cand[kMaxK];
     bool empty = false;
-    for (int u = 0; u < k_; ++u) {
-        cand[u] = hc[u];
-        res_->candidates[u] = hc[u];
-        if (hc[u] == 0) empty = true;
+    // Unlabeled query without refinement: |C(u)| = #{v : deg(v) >= deg_Q(u)} is non-increasing
+    // in deg_Q(u), so the order (max d_M, min |C(u)|, max deg, min id) is the order by (max d_M,
+    // max deg, min id) and C(u) is empty iff deg_Q(u) > max degree: the counts are not needed
+    // before the search, and are read back with the result (one host sync fewer per match).
+    deferred_counts_ = !plan_.use_labels && opts_.refine_rounds == 0;
+    if (deferred_counts_) {
+        for (int u = 0; u < k_; ++u) {
+            cand[u] = (uint64_t)(kMaxK + 1 - plan_.qdeg[u]);  // order-equivalent proxy
+            if (plan_.qdeg[u] > g_.max_degree) empty = true;
+        }
+    } else {
+        unsigned long long hc[kMaxK];
+        GSM_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, s_));
+        GSM_CUDA(cudaStreamSynchronize(s_));
+        for (int u = 0; u < k_; ++u) {
+            cand[u] = hc[u];
+            res_->candidates[u] = hc[u];
+            if (hc[u] == 0) empty = true;
+        }
     }
     // ---- query order with the exact |C(u)|
     compute_order(&plan_, cand, opts_.root_subset ? 0 : -1);
@@ -314,35 +329,6 @@ void Matcher::run() {
     GSM_CUDA(cudaMemsetAsync(stats_.p, 0, sizeof(unsigned long long) * 5 * (kMaxK + 1), s_));
     for (int w = 1; w < k_; ++w) lv_[w]->stats = stats_.p + 5 * w;
 
-    size_t free_b = 0, total_b = 0;
-    GSM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    {   // allocatable = free + what the stream-ordered pool holds but nobody uses + this graph's
-        // cached frontier buffers (they are released and re-grown to the new chunk sizes);
-        // default budget = min(total/4, 0.9 x allocatable), stable across calls
-        int dev = 0;
-        GSM_CUDA(cudaGetDevice(&dev));
-        cudaMemPool_t pool;
-        GSM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-        uint64_t reserved = 0, used = 0;
-        GSM_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
-        GSM_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
-        double cached = 0;
-        for (int w = 2; w <= k_; ++w) cached += sizeof(int32_t) * (double)lv_[w]->rows.n;
-        const double avail = 0.9 * ((double)free_b + (double)(reserved > used ? reserved - used : 0) + cached);
-        budget_ = opts_.mem_budget_bytes ? (int64_t)opts_.mem_budget_bytes
-                                         : (int64_t)std::min((double)total_b / 4.0, avail);
-    }
-    compress_ = ((opts_.flags & GSM_FLAG_COMPRESSED_PARTIALS) || knobs().compress > 0) && knobs().compress != 0;
-    res_->compressed = compress_ ? 1 : 0;
-    // per-width share of the budget for frontiers of width 2..k (k only when enumerating)
-    const int nfront = count_mode_ ? std::max(0, k_ - 2) : k_ - 1;
-    for (int w = 2; w <= k_; ++w) {
-        const int64_t share = nfront > 0 ? budget_ / nfront : budget_;
-        // stored partial result + its row plan (rbeg/rlen/P, piv, per-backward segments)
-        const int64_t per_row = (compress_ && w < k_ ? 8 : 4 * w) + 8 * 3 + 1 + 1 + 12 * (w - 1);
-        lv_[w]->cap_rows = std::max<int64_t>(share / per_row, 1);
-    }
-
     uint64_t found = 0;
     if (k_ == 1) {
         found = (uint64_t)R0;
@@ -370,18 +356,35 @@ void Matcher::run() {
         res_->num_chunks++;
         // roots whose N+(u) exceeds the per-CTA tables: the breadth-first path (same counter)
         if (cr.n_over > 0) process(1, plain(over.p, 1), cr.n_over);
-        found = read_scalar(final_count_.p, s_);
     } else if (R0 > 0) {
         process(1, plain(lv_[1]->rows.p, 1), R0);
-        if (count_mode_) found = read_scalar(final_count_.p, s_);
-        else found = (uint64_t)arena_rows_;
     }
+    // one host sync for the result: final count, per-level stats, deferred |C(u)|
+    // (pinned staging, so the copies are truly asynchronous and share the one sync)
+    std::vector<unsigned long long> hv(Workspace::kPin, 0);
+    unsigned long long* hp = ws_.pinned();
+    if (!hp) hp = hv.data();  // pageable fallback: each copy then blocks by itself
+    unsigned long long *hfound = hp, *hcand = hp + 1, *hstat = hp + 1 + kMaxK;
+    const size_t nstat = 5 * (kMaxK + 1);
+    *hfound = 0;
+    if (k_ > 1 && count_mode_ && R0 > 0)
+        GSM_CUDA(cudaMemcpyAsync(hfound, final_count_.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s_));
+    if (k_ > 1)
+        GSM_CUDA(cudaMemcpyAsync(hstat, stats_.p, sizeof(unsigned long long) * nstat, cudaMemcpyDeviceToHost, s_));
+    if (deferred_counts_)
+        GSM_CUDA(cudaMemcpyAsync(hcand, counts.p, sizeof(unsigned long long) * kMaxK, cudaMemcpyDeviceToHost, s_));
+    {
+        const auto ts = Clock::now();
+        GSM_CUDA(cudaStreamSynchronize(s_));
+        g_trace.sync_ms += ms_since(ts);
+        g_trace.syncs++;
+    }
+    if (deferred_counts_)
+        for (int u = 0; u < k_; ++u) res_->candidates[u] = hcand[u];
+    if (k_ > 1 && R0 > 0) found = count_mode_ ? (uint64_t)*hfound : (uint64_t)arena_rows_;
+    std::vector<unsigned long long> hs(hstat, hstat + nstat);
     // per-level stats -> result + algorithmic bytes of the expand kernel
     if (k_ > 1) {
-        std::vector<unsigned long long> hs(5 * (kMaxK + 1));
-        GSM_CUDA(cudaMemcpyAsync(hs.data(), stats_.p, sizeof(unsigned long long) * hs.size(),
-                                 cudaMemcpyDeviceToHost, s_));
-        GSM_CUDA(cudaStreamSynchronize(s_));
         double eb = 0;
         for (int w = 1; w < k_; ++w) {
             const unsigned long long* st = hs.data() + 5 * w;
@@ -430,6 +433,42 @@ void Matcher::run() {
     res_->ms_finalize = (float)ms_since(t0);
     rec_.finish();
     res_->ms_total = (float)ms_since(t_all);
+}
+
+void Matcher::ensure_caps() {
+    // frontier capacities (A7 chunking), computed on first use: matches that never expand a
+    // breadth-first level (clique path, k = 1) skip the memory queries
+    if (caps_ready_) return;
+    caps_ready_ = true;
+    size_t free_b = 0, total_b = 0;
+    GSM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    {   // allocatable = free + what the stream-ordered pool holds but nobody uses + this graph's
+        // cached frontier buffers (they are released and re-grown to the new chunk sizes);
+        // default budget = min(total/4, 0.9 x allocatable), stable across calls
+        int dev = 0;
+        GSM_CUDA(cudaGetDevice(&dev));
+        cudaMemPool_t pool;
+        GSM_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t reserved = 0, used = 0;
+        GSM_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+        GSM_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+        double cached = 0;
+        for (int w = 2; w <= k_; ++w) cached += sizeof(int32_t) * (double)lv_[w]->rows.n;
+        const double avail = 0.9 * ((double)free_b + (double)(reserved > used ? reserved - used : 0) + cached);
+        budget_ = opts_.mem_budget_bytes ? (int64_t)opts_.mem_budget_bytes
+                                         : (int64_t)std::min((double)total_b / 4.0, avail);
+    }
+    compress_ = ((opts_.flags & GSM_FLAG_COMPRESSED_PARTIALS) || knobs().compress > 0) && knobs().compress != 0;
+    res_->compressed = compress_ ? 1 : 0;
+    // per-width share of the budget for frontiers of width 2..k (k only when enumerating)
+    const int nfront = count_mode_ ? std::max(0, k_ - 2) : k_ - 1;
+    for (int w = 2; w <= k_; ++w) {
+        const int64_t share = nfront > 0 ? budget_ / nfront : budget_;
+        // stored partial result + its row plan (rbeg/rlen/P, piv, per-backward segments)
+        const int64_t per_row = (compress_ && w < k_ ? 8 : 4 * w) + 8 * 3 + 1 + 1 + 12 * (w - 1);
+        lv_[w]->cap_rows = std::max<int64_t>(share / per_row, 1);
+    }
+
 }
 
 void Matcher::process(int w, const Frontier& F, int64_t R) {
@@ -632,6 +671,7 @@ void Matcher::process_pair(int w, const Frontier& F, int64_t R) {
 
 void Matcher::process_generic(int w, const Frontier& F, int64_t R) {
     if (R <= 0) return;
+    ensure_caps();
     LevelBufs& B = *lv_[w];
     const LevelPlan& L = lplan_[w];
     // per-row pivot choice and admissible segment

@@ -34,8 +34,21 @@ struct Workspace {
     DevBuf<uint8_t> ck_tmp;
     DevBuf<unsigned long long> ck_bucket, ck_sched;
     DevBuf<int> ck_dmax;
+    // pinned host staging for the end-of-match read-back (several D2H copies, one sync)
+    unsigned long long* pin = nullptr;
+    static constexpr size_t kPin = 1 + kMaxK + 5 * (kMaxK + 1);
+    unsigned long long* pinned() {
+        if (!pin && cudaMallocHost(&pin, sizeof(unsigned long long) * kPin) != cudaSuccess) {
+            (void)cudaGetLastError();
+            pin = nullptr;
+        }
+        return pin;
+    }
     Workspace() : lv(kMaxK + 1) {
         for (auto& p : lv) p.reset(new LevelBufs());
+    }
+    ~Workspace() {
+        if (pin) cudaFreeHost(pin);
     }
 };
 

@@ -42,8 +42,13 @@ def parse_args():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--e2e-steps", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
+    p.add_argument("--cpu-seconds", type=float, default=8.0, help="oracle sample budget per pass (cpu_baseline)")
     p.add_argument("--refine-rounds", type=int, default=0, help="NE filter rounds (Alg. 1 lines 7-8)")
+    p.add_argument("--mode", default="count", choices=["count", "enumerate"],
+                   help="enumerate: rows materialised, sorted (device-timed) and copied D2H (e2e)")
+    p.add_argument("--clique", type=int, default=1, help="0: K3/K4 take the breadth-first path (GSM_CLIQUE=0)")
+    p.add_argument("--lookahead", type=int, default=0, help="k-look-ahead depth (0/1/2)")
+    p.add_argument("--compressed", action="store_true", help="compressed partial results")
     return p.parse_args()
 
 
@@ -153,7 +158,7 @@ def load_peaks():
 
 KERNELS_OF = {"expand": ["k_expand", "k_count_walk"], "tail": ["k_tail", "k_tail_block"],
               "clique": ["k_clique_cta", "k_clique_warp"], "filter": ["k_filter"],
-              "plan": ["k_plan_rows"], "roots": ["k_root_count", "k_root_write"]}
+              "plan": ["k_plan_rows", "k_plan_rows_grp"], "roots": ["k_root_count", "k_root_write"]}
 
 
 def ncu_traffic(workload: str, kind: str, launches_per_step: float):
@@ -196,24 +201,54 @@ def oracle_pass(g, queries, roots):
     return uni, time.perf_counter() - t0
 
 
+def _pass_child(conn, g, queries, roots):
+    conn.send(oracle_pass(g, queries, roots))
+    conn.close()
+
+
+def oracle_pass_bounded(g, queries, roots, limit_s: float):
+    """oracle_pass in a forked child (the graph is shared copy-on-write), killed after
+    limit_s: per-root DFS cost is heavy-tailed (one R-MAT hub root can take hours), so a
+    calibration pass must be interruptible without touching the oracle.  None on timeout."""
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    a, b = ctx.Pipe(duplex=False)
+    p = ctx.Process(target=_pass_child, args=(b, g, queries, roots), daemon=True)
+    p.start()
+    b.close()
+    res = a.recv() if a.poll(limit_s) else None
+    if p.is_alive():
+        p.kill()
+    p.join()
+    return res
+
+
 def oracle_sample(g, queries, target_s: float):
-    """A FIXED evenly strided root sample sized so one oracle pass takes about target_s
-    seconds: start at 16 roots, grow geometrically while a pass is < target/3, shrink if a
-    pass overshoots 1.5 x target.  Every calibration pass is bounded by ~1.5 x target, so
-    the whole calibration costs a few targets.  Returns (roots, unique, seconds, threads)."""
+    """A FIXED evenly strided root sample sized so one oracle pass takes about target_s:
+    start at 16 roots, grow geometrically while a pass is < target/3, shrink on a pass
+    over 1.5 x target (such a pass is killed at that limit, so calibration stays bounded
+    even when the sample hits a hub).  Returns (roots, unique, seconds, threads)."""
     import oracle
     n = g.num_nodes
     cnt = 16
-    for _ in range(12):
+    best = None
+    for _ in range(16):
         roots = strided_roots(n, cnt)
-        uni, dt = oracle_pass(g, queries, roots)
-        if dt > 1.5 * target_s and cnt > 1:
-            cnt = max(1, int(cnt * target_s / dt))
+        res = oracle_pass_bounded(g, queries, roots, 1.5 * target_s)
+        if res is None:  # over the limit: shrink, and never grow past this size again
+            cnt = max(1, cnt // 2) if cnt > 1 else 1
+            if cnt == 1 and best is None:
+                roots = strided_roots(n, 1)
+                uni, dt = oracle_pass(g, queries, roots)
+                return roots, uni, dt, oracle.num_threads()
             continue
+        uni, dt = res
+        best = (roots, uni, dt)
         if dt < target_s / 3 and cnt < n:
             cnt = min(n, int(cnt * min(8.0, max(1.5, 0.9 * target_s / max(dt, 1e-4)))))
             continue
         break
+    roots, uni, dt = best
     return roots, uni, dt, oracle.num_threads()
 
 
@@ -242,7 +277,7 @@ def run_reference(args, world, rank):
         oracle_pass(g, w.queries, roots)
     tot = 0.0
     times = []
-    for _ in range(args.steps):
+    for _ in range(args.steps):  # same deterministic sample as the accepted calibration pass
         uni, dt = oracle_pass(g, w.queries, roots)
         tot += uni
         times.append(dt)
@@ -261,9 +296,13 @@ def run_reference(args, world, rank):
     print(json.dumps(out), flush=True)
 
 
-def config_of(w, g, refine_rounds=0):
+def config_of(w, g, refine_rounds=0, args=None):
+    extra = {}
+    if args is not None:
+        extra = {"match_mode": args.mode, "clique_path": bool(args.clique), "lookahead": args.lookahead,
+                 "compressed_partials": bool(args.compressed)}
     return {"workload": f"{w.name} (BASELINE configs[{w.config_index}]): {w.description}",
-            "refine_rounds": refine_rounds,
+            "refine_rounds": refine_rounds, **extra,
             "graph": {"name": g.name, "num_nodes": g.num_nodes, "directed_edges": g.nnz,
                       "csr_bytes": int(g.offsets.nbytes + g.cols.nbytes + (0 if g.labels is None else g.labels.nbytes))},
             "queries": [q.name for q in w.queries],
@@ -284,6 +323,8 @@ def run_ours(args, world, rank, local, dist):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if not args.clique:
+        os.environ["GSM_CLIQUE"] = "0"  # read by the library at every gsm_match
     w = workloads.get(args.workload)
     if dist is not None:  # rank 0 generates (all host cores) and fills the on-disk cache; the others load it
         if rank == 0:
@@ -303,18 +344,33 @@ def run_ours(args, world, rank, local, dist):
 
     per_query = {}
 
-    def step(flags, G_=None):
+    enumerate_ = args.mode == "enumerate"
+    extra_flags = gsm.GSM_FLAG_COMPRESSED_PARTIALS if args.compressed else 0
+    host_rows = {}  # e2e (enumerate): pinned destination of each query's rows
+
+    def step(flags, G_=None, d2h=False):
         G_ = G_ or G
         tot_all = tot_unique = launches = 0
         profs = []
         for q in w.queries:
-            r = gsm.gsm_match(G_, q.num_nodes, q.edges, q.labels, mode=gsm.GSM_MODE_COUNT, flags=flags,
-                              shard_index=rank, num_shards=world, mem_budget_bytes=w.mem_budget_bytes, stream=sptr,
-                              refine_rounds=args.refine_rounds)
+            r = gsm.gsm_match(G_, q.num_nodes, q.edges, q.labels,
+                              mode=gsm.GSM_MODE_ENUMERATE if enumerate_ else gsm.GSM_MODE_COUNT,
+                              flags=flags | extra_flags, shard_index=rank, num_shards=world,
+                              mem_budget_bytes=w.mem_budget_bytes, stream=sptr, refine_rounds=args.refine_rounds,
+                              lookahead=args.lookahead)
             tot_all += r.count
             tot_unique += r.count_unique
             launches += r.kernel_launches
             profs.append(r.prof)
+            if enumerate_:
+                if d2h and r.num_rows:  # rows to pinned host memory through the C ABI
+                    hb = host_rows.get(q.name)
+                    if hb is None or hb.numel() < r.num_rows * r.width:
+                        hb = torch.empty(r.num_rows * r.width, dtype=torch.int32).pin_memory()
+                        host_rows[q.name] = hb
+                    gsm.gsm_result_copy_rows(r, hb, False)
+                    host_rows[q.name + ":bytes"] = r.num_rows * r.width * 4
+                r.free()
             if G_ is not G:
                 continue  # e2e steps (fresh graph each step) do not overwrite the resident-graph stats
             per_query[q.name] = {"count": r.count, "unique": r.count_unique, "automorphisms": r.automorphisms,
@@ -388,7 +444,7 @@ def run_ours(args, world, rank, local, dist):
         # one untimed end-to-end step first (the W warm-up rule): the first upload of a fresh
         # graph maps the memory pool's pages (measured ~120 ms extra on R-MAT-24)
         G2 = gsm.gsm_load_graph(g.num_nodes, off_h, cols_h, lab_h, device=local, stream=sptr)
-        step(0, G2)
+        step(0, G2, d2h=True)
         G2.free()
         barrier()
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -397,7 +453,7 @@ def run_ours(args, world, rank, local, dist):
         e_cnt = 0
         for _ in range(args.e2e_steps):
             G2 = gsm.gsm_load_graph(g.num_nodes, off_h, cols_h, lab_h, device=local, stream=sptr)
-            e_cnt = step(0, G2)[1]
+            e_cnt = step(0, G2, d2h=True)[1]
             G2.free()
         ev1.record(stream)
         ev1.synchronize()
@@ -410,8 +466,9 @@ def run_ours(args, world, rank, local, dist):
             dist.all_reduce(c)
             e_cnt = int(c.item())
         h2d = (g.offsets.nbytes + g.cols.nbytes + (0 if g.labels is None else g.labels.nbytes)) * world
+        rows_d2h = sum(v for k, v in host_rows.items() if k.endswith(":bytes"))
         e2e = {"value": e_cnt / (e_ms / 1000.0), "unit": METRIC, "ms_per_step": e_ms,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * len(w.queries) * world)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(8 * len(w.queries) * world + rows_d2h)}
     G.free()
 
     if rank != 0:
@@ -441,7 +498,7 @@ def run_ours(args, world, rank, local, dist):
            "per_rank_ms": per_rank_ms, "imbalance_max_over_mean": max(per_rank_ms) / (sum(per_rank_ms) / len(per_rank_ms)),
            "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-           "config": config_of(w, g, args.refine_rounds),
+           "config": config_of(w, g, args.refine_rounds, args),
            "counts_per_step": {"all": c_all, "unique": c_uni},
            "all_per_s": c_all / (ms / 1000.0),
            "query_ms": ms, "per_query_rank0": per_query, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}

@@ -104,6 +104,9 @@ struct Knobs {
     int expand_td = 512;      // GSM_EXPAND_TD (clamped 128..2048)
     int expand_ilp = 1;       // GSM_EXPAND_ILP (1, 2 or 4)
     int trace = 0;            // GSM_TRACE: 1 host trace, 2 per-phase cycle counters
+    int member_hub = 1;       // GSM_MEMBER_HUB: pair-tail membership tests of two hubs by the hub bitmap
+    int member_swap = 64;     // GSM_MEMBER_SWAP: segments longer than this may search in N(v) (0 = never)
+    int plan_groups = 1;      // GSM_PLAN_GROUPS: row plans by lane groups (one lane per backward neighbour)
     int compress = -1;        // GSM_COMPRESS: 1/0 force the compressed partial layout on/off (-1 = flag)
     int lookahead = -1;       // GSM_LOOKAHEAD: overrides gsm_match_opts.lookahead when >= 0
     int hub_bits = 32768;     // GSM_HUB_BITS: H of the hub adjacency bitmap built at load (0 = none)

@@ -70,6 +70,9 @@ void load_knobs() {
     k.trace = env_or("GSM_TRACE", 0);
     k.lookahead = env_or("GSM_LOOKAHEAD", -1);
     k.compress = env_or("GSM_COMPRESS", -1);
+    k.plan_groups = env_or("GSM_PLAN_GROUPS", k.plan_groups);
+    k.member_hub = env_or("GSM_MEMBER_HUB", k.member_hub);
+    k.member_swap = env_or("GSM_MEMBER_SWAP", k.member_swap);
     k.hub_bits = std::max(0, env_or("GSM_HUB_BITS", k.hub_bits)) & ~31;
     k.clique_hub = env_or("GSM_CLIQUE_HUB", k.clique_hub);
     k.clique_hub_ratio = env_or("GSM_CLIQUE_HUB_RATIO", k.clique_hub_ratio);

@@ -75,6 +75,9 @@ struct LevelPlan {
     int32_t keyed;
     int32_t key_base;
     int32_t idmask;
+    // keyed lists: key of each backward neighbour's image in OTHER lists = its query label <<
+    // idbits (-1: unknown / not keyed -> plain ids); lets a membership test search the shorter list
+    int32_t bkey[kMaxK];
     // k-look-ahead (DESIGN R17): the unmapped query neighbours of π[i]
     int32_t la_depth;    // 0 (off), 1 or 2
     int32_t nla;

@@ -525,10 +525,93 @@ __global__ void __launch_bounds__(kThreads) k_plan_rows(const Frontier F, int64_
     }
 }
 
+// Lane-group variant: a group of G = 2^ceil(log2 |B(i)|) lanes per row, lane q of the
+// group owns backward neighbour q — the |B(i)| independent segment searches of a row run in
+// parallel instead of as one thread's dependent chain (more loads in flight; the searches
+// are latency-bound), the pivot choice is a shuffle-min inside the group.
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_plan_rows_grp(const Frontier F, int64_t R, LevelPlan L,
+                                                            const int64_t* __restrict__ off,
+                                                            const int32_t* __restrict__ cols,
+                                                            const int32_t* __restrict__ up, int64_t n,
+                                                            int64_t* __restrict__ rbeg, int64_t* __restrict__ rlen,
+                                                            uint8_t* __restrict__ rpiv, int64_t* __restrict__ cbeg,
+                                                            int32_t* __restrict__ clen) {
+    const int nb = L.nb;
+    const int q = threadIdx.x & (G - 1);
+    const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+    const int64_t iters = (R + ngroups - 1) / ngroups;  // uniform trip count: shuffles stay converged
+    int32_t buf[kMaxK];
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t r = gid + it * ngroups;
+        const bool live = r < R && q < nb;
+        int64_t lov = -1, hiv = n, s0 = 0, t0 = 0;
+        int32_t a = 0;
+        if (r < R) {
+            const int32_t* row = frontier_row(F, r, buf);
+            for (int x = 0; x < L.nlo; ++x) lov = max(lov, (int64_t)row[L.lo[x]]);
+            for (int x = 0; x < L.nhi; ++x) hiv = min(hiv, (int64_t)row[L.hi[x]]);
+            if (live) a = row[L.bpos[q]];
+        }
+        const bool empty = lov + 1 >= hiv;
+        int64_t est = INT64_MAX;
+        if (live) {
+            if (L.keyed) {
+                s0 = off[a];
+                t0 = off[a + 1];
+                if (!empty) {
+                    const int64_t klo = (int64_t)L.key_base + lov + 1, khi = (int64_t)L.key_base + hiv;
+                    s0 = lower_bound_cols(cols, s0, t0, klo);
+                    t0 = lower_bound_cols(cols, s0, t0, khi);
+                } else {
+                    t0 = s0;
+                }
+                est = t0 - s0;
+            } else {
+                admissible_segment(off, cols, up, n, a, lov, hiv, false, s0, t0);
+                est = t0 - s0;
+            }
+        }
+        // pivot = shortest (estimated) segment, lowest q on ties
+        int64_t best = est;
+        int bq = q;
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+            const int64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+            if (ob < best || (ob == best && oq < bq)) { best = ob; bq = oq; }
+        }
+        if (live && !L.keyed) {  // exact segments (ID bounds folded in), as k_plan_rows
+            admissible_segment(off, cols, up, n, a, lov, hiv, !empty, s0, t0);
+            if (empty) t0 = s0;
+        }
+        if (live) {
+            cbeg[r * nb + q] = s0;
+            clen[r * nb + q] = (int32_t)(t0 - s0);
+            if (q == bq) {
+                rbeg[r] = s0;
+                rlen[r] = t0 - s0;
+                rpiv[r] = (uint8_t)bq;
+            }
+        }
+    }
+}
+
 void launch_plan_rows(const DevGraph& g, const Frontier& F, int64_t R, const LevelPlan& L, int64_t* rbeg,
                       int64_t* rlen, uint8_t* rpiv, int64_t* cbeg, int32_t* clen, cudaStream_t s) {
-    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, L.keyed ? g.lkeys : g.cols, g.up, g.n, rbeg, rlen,
-                                                 rpiv, cbeg, clen);
+    const int32_t* cols = L.keyed ? g.lkeys : g.cols;
+    const int nb = L.nb;
+    if (knobs().plan_groups && nb >= 2 && nb <= 8) {
+        const int G = nb <= 2 ? 2 : (nb <= 4 ? 4 : 8);
+        const int grid = grid_for(R * G, kThreads, 148 * 8);
+        if (G == 2) k_plan_rows_grp<2><<<grid, kThreads, 0, s>>>(F, R, L, g.off, cols, g.up, g.n, rbeg, rlen, rpiv, cbeg, clen);
+        else if (G == 4) k_plan_rows_grp<4><<<grid, kThreads, 0, s>>>(F, R, L, g.off, cols, g.up, g.n, rbeg, rlen, rpiv, cbeg, clen);
+        else k_plan_rows_grp<8><<<grid, kThreads, 0, s>>>(F, R, L, g.off, cols, g.up, g.n, rbeg, rlen, rpiv, cbeg, clen);
+        GSM_LAUNCH("k_plan_rows_grp");
+        return;
+    }
+    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, cols, g.up, g.n, rbeg, rlen, rpiv, cbeg, clen);
     GSM_LAUNCH("k_plan_rows");
 }
 
@@ -638,6 +721,27 @@ __device__ __forceinline__ bool in_sorted(const int32_t* __restrict__ a, int len
     }
     ++probes;
     return *base == v;
+}
+
+// v ∈ N(f), where seg/len is the admissible segment of f's list and v lies in its key range
+// (same label and ID interval): one hub-bitmap bit when both are hubs; otherwise, when f's
+// segment is long and v's whole list is shorter, f's key searched in N(v) (the graph is
+// symmetric); else v's key searched in the segment.
+__device__ __forceinline__ bool member(const MemberCtx& m, const int32_t* __restrict__ cols,
+                                       const int32_t* seg, int len, int32_t keyv, int32_t v, int32_t f,
+                                       int32_t keyf, unsigned& probes) {
+    if (len <= 0) return false;
+    if (m.hub_bits && v >= m.hub_base && f >= m.hub_base) {
+        const int lo = min(v, f) - m.hub_base, hi = max(v, f) - m.hub_base;
+        ++probes;
+        return (__ldg(hub_row(m.hub_bits, m.hub_words, lo) + (hi >> 5)) >> (hi & 31)) & 1u;
+    }
+    if (m.swap_min > 0 && len > m.swap_min && keyf >= 0) {
+        const int64_t b = m.off[v], e = m.off[v + 1];
+        probes += 2;
+        if (e - b < len) return in_sorted(cols + b, (int)(e - b), keyf | f, probes);
+    }
+    return in_sorted(seg, len, keyv, probes);
 }
 
 struct MaxOp {
@@ -1568,7 +1672,8 @@ __global__ void __launch_bounds__(kThreads) k_pair(PairArgs a, LevelPlan Lp, Lev
                 for (int t = 0; t < Lp.ninj && ok; ++t) ok = v != row[Lp.inj[t]];
                 for (int t = 0; t < Lp.nb && ok; ++t)
                     if (t != piv)
-                        ok = in_sorted(a.colsp + a.pcbeg[r * Lp.nb + t], a.pclen[r * Lp.nb + t], Lp.key_base | v, probes);
+                        ok = member(a.mem, a.colsp, a.colsp + a.pcbeg[r * Lp.nb + t], a.pclen[r * Lp.nb + t],
+                                    Lp.key_base | v, v, row[Lp.bpos[t]], Lp.bkey[t], probes);
                 cp += ok;
                 if (ok && a.need_both) {  // also a candidate of q?
                     bool o2 = true;
@@ -1591,7 +1696,8 @@ __global__ void __launch_bounds__(kThreads) k_pair(PairArgs a, LevelPlan Lp, Lev
                 for (int t = 0; t < Lq.ninj && ok; ++t) ok = v != row[Lq.inj[t]];
                 for (int t = 0; t < Lq.nb && ok; ++t)
                     if (t != piv)
-                        ok = in_sorted(a.colsq + a.qcbeg[r * Lq.nb + t], a.qclen[r * Lq.nb + t], Lq.key_base | v, probes);
+                        ok = member(a.mem, a.colsq, a.colsq + a.qcbeg[r * Lq.nb + t], a.qclen[r * Lq.nb + t],
+                                    Lq.key_base | v, v, row[Lq.bpos[t]], Lq.bkey[t], probes);
                 cq += ok;
             }
         }
@@ -1643,7 +1749,8 @@ __global__ void __launch_bounds__(kThreads) k_pair_thread(PairArgs a, LevelPlan 
             for (int t = 0; t < Lp.ninj && ok; ++t) ok = v != row[Lp.inj[t]];
             for (int t = 0; t < Lp.nb && ok; ++t)
                 if (t != ppv)
-                    ok = in_sorted(a.colsp + a.pcbeg[r * Lp.nb + t], a.pclen[r * Lp.nb + t], Lp.key_base | v, probes);
+                    ok = member(a.mem, a.colsp, a.colsp + a.pcbeg[r * Lp.nb + t], a.pclen[r * Lp.nb + t],
+                                Lp.key_base | v, v, row[Lp.bpos[t]], Lp.bkey[t], probes);
             cp += ok;
             if (ok && a.need_both) {
                 bool o2 = true;
@@ -1665,7 +1772,8 @@ __global__ void __launch_bounds__(kThreads) k_pair_thread(PairArgs a, LevelPlan 
             for (int t = 0; t < Lq.ninj && ok; ++t) ok = v != row[Lq.inj[t]];
             for (int t = 0; t < Lq.nb && ok; ++t)
                 if (t != qpv)
-                    ok = in_sorted(a.colsq + a.qcbeg[r * Lq.nb + t], a.qclen[r * Lq.nb + t], Lq.key_base | v, probes);
+                    ok = member(a.mem, a.colsq, a.colsq + a.qcbeg[r * Lq.nb + t], a.qclen[r * Lq.nb + t],
+                                Lq.key_base | v, v, row[Lq.bpos[t]], Lq.bkey[t], probes);
             cq += ok;
         }
         items += plen + qlen;

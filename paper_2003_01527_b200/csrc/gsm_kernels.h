@@ -165,8 +165,18 @@ void launch_gather_rows(const Frontier& F, const int64_t* idx, int64_t n, int32_
 
 // Pair tail (COUNT mode): positions p = k-2 and q = k-1 not adjacent in Q and without an ID
 // condition between them: count(r) = |Cp(r)| |Cq(r)| - |Cp(r) ∩ Cq(r)| per row r of width k-2.
+// exact adjacency test v ∈ N(f) for v already inside the admissible range of f's segment:
+// hub bitmap when both are hubs, else binary search in the shorter of seg and N(v)
+struct MemberCtx {
+    const int64_t* off = nullptr;
+    const uint32_t* hub_bits = nullptr;
+    int32_t hub_base = 0, hub_words = 0;
+    int32_t swap_min = 0;   // segments longer than this may search f in N(v) instead (0 = never)
+};
+
 struct PairArgs {
     Frontier F;
+    MemberCtx mem;
     int64_t R;
     const int64_t *pbeg, *plen, *pcbeg;  // k_plan_rows of position p
     const uint8_t* ppiv;

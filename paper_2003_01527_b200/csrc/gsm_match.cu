@@ -238,6 +238,12 @@ void Matcher::run() {
             L.idmask = (int32_t)((1u << g_.idbits) - 1u);
             // the label is implied by the key range; the degree by |B(i)| unless NE-refined
             L.check_mask = (opts_.refine_rounds > 0 || plan_.qdeg[L.qv] > L.nb) ? 1 : 0;
+            for (int q = 0; q < L.nb; ++q) {
+                const uint32_t lb = plan_.qlabel[plan_.order[L.bpos[q]]];
+                L.bkey[q] = lb <= g_.max_label ? (int32_t)(lb << g_.idbits) : -1;
+            }
+        } else if (plan_.use_labels && g_.lkeys) {
+            for (int q = 0; q < L.nb; ++q) L.bkey[q] = -1;  // plain list of an unkeyed label: no swap
         }
     }
 
@@ -644,6 +650,11 @@ void Matcher::process_pair(int w, const Frontier& F, int64_t R) {
     a.colsq = lq_.keyed ? g_.lkeys : g_.cols;
     a.cmask = cmask_.p;
     a.need_both = !(plan_.use_labels && plan_.qlabel[Lp.qv] != plan_.qlabel[lq_.qv]);
+    a.mem.off = g_.off;
+    a.mem.hub_bits = knobs().member_hub ? g_.hub_bits : nullptr;
+    a.mem.hub_base = g_.hub_base;
+    a.mem.hub_words = g_.hub_words;
+    a.mem.swap_min = knobs().member_swap;
     a.count = final_count_.p;
     ws_.sched.ensure(1, s_);
     GSM_CUDA(cudaMemsetAsync(ws_.sched.p, 0, sizeof(unsigned long long), s_));

@@ -264,6 +264,7 @@ LevelPlan make_level_plan(const QueryPlan& p, int i, bool count_only) {
     L.keyed = 0;
     L.key_base = 0;
     L.idmask = -1;
+    for (int q = 0; q < kMaxK; ++q) L.bkey[q] = 0;  // plain lists: a vertex's key is its id
     return L;
 }
 

@@ -199,12 +199,22 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
         G.free()
 
 
-@pytest.mark.parametrize("pair", ["1", "warp", "0"])
+@pytest.mark.parametrize("pair", ["1", "warp", "0", "plan_thread", "nohub", "swap1", "swap1_warp"])
 def test_pair_tail(pair, monkeypatch):
     """COUNT mode with the last two positions an independent pair (k_pair: |Cp||Cq| - |Cp∩Cq|)
     against the oracle's count, labeled and unlabeled, with and without symmetry; "0" =
     the pair ordering disabled (GSM_PAIR_TAIL=0) on the same inputs; "warp" = every row through
     the warp-per-row kernel (no thread-per-row pass)."""
+    if pair == "plan_thread":  # row plans by one thread per row instead of lane groups
+        monkeypatch.setenv("GSM_PLAN_GROUPS", "0")
+    # membership tests: these small graphs are all hubs by default (bitmap tests); "nohub" = binary
+    # searches only; "swap1" = search the image in N(v) whenever v's list is the shorter one
+    if pair in ("nohub", "swap1", "swap1_warp"):
+        monkeypatch.setenv("GSM_HUB_BITS", "0")
+    if pair.startswith("swap1"):
+        monkeypatch.setenv("GSM_MEMBER_SWAP", "1")
+    if pair == "swap1_warp":
+        monkeypatch.setenv("GSM_PAIR_THREAD_MAX", "0")
     monkeypatch.setenv("GSM_PAIR_TAIL", "0" if pair == "0" else "1")
     if pair == "warp":
         monkeypatch.setenv("GSM_PAIR_THREAD_MAX", "0")

@@ -376,6 +376,7 @@ def run_ours(args, world, rank, local, dist):
             per_query[q.name] = {"count": r.count, "unique": r.count_unique, "automorphisms": r.automorphisms,
                                  "order": r.order, "candidates": r.candidates, "level_work": r.level_work,
                                  "level_rows": r.level_rows, "chunks": r.num_chunks,
+                                 "level_frontier_bytes": r.level_frontier_bytes, "compressed": r.compressed,
                                  "ms": {k: round(v, 3) for k, v in r.ms.items()},
                                  "kernel_ms": {k: round(v["ms"], 3) for k, v in r.prof.items()}}
         return tot_all, tot_unique, launches, profs

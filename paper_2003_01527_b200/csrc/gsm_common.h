@@ -112,6 +112,7 @@ struct Knobs {
     int hub_bits = 32768;     // GSM_HUB_BITS: H of the hub adjacency bitmap built at load (0 = none)
     int clique_hub = 1;       // GSM_CLIQUE_HUB: clique rows of a hub pivot by bitmap lookups
     int clique_hub_ratio = 64;  // GSM_CLIQUE_HUB_RATIO: lookups when 32 nj <= ratio |N+(S[i])|
+    int order = 0;            // GSM_ORDER (read at gsm_load_graph): 0 = rank by (degree, id), 1 = approximate degeneracy
 };
 void load_knobs();
 const Knobs& knobs();

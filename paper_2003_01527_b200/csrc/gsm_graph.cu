@@ -76,6 +76,7 @@ void load_knobs() {
     k.hub_bits = std::max(0, env_or("GSM_HUB_BITS", k.hub_bits)) & ~31;
     k.clique_hub = env_or("GSM_CLIQUE_HUB", k.clique_hub);
     k.clique_hub_ratio = env_or("GSM_CLIQUE_HUB_RATIO", k.clique_hub_ratio);
+    k.order = env_or("GSM_ORDER", k.order);
     g_knobs = k;
 }
 
@@ -147,14 +148,80 @@ __global__ void k_degree_keys(const int64_t* __restrict__ off, int64_t n, uint64
     if ((threadIdx.x & 31) == 0) atomicMax(maxdeg, local);
 }
 
-__global__ void k_permutation(const uint64_t* __restrict__ sorted, int64_t n, int32_t* new2old, int32_t* old2new,
-                              int64_t* newdeg) {
+__global__ void k_permutation(const uint64_t* __restrict__ sorted, const int64_t* __restrict__ off, int64_t n,
+                              int32_t* new2old, int32_t* old2new, int64_t* newdeg) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         uint64_t k = sorted[p];
         int32_t old = (int32_t)(k & 0xffffffffu);
         new2old[p] = old;
         old2new[old] = (int32_t)p;
-        newdeg[p] = (int64_t)(k >> 32);
+        newdeg[p] = off[old + 1] - off[old];
+    }
+}
+
+// ---------------------------------------------------------------- approximate degeneracy order
+// (GSM_ORDER=1; any strict total order ≺ is valid, SURVEY §8(c) amb. 9).  Peeling in rounds:
+// every remaining vertex whose remaining degree is <= (1 + eps) x the remaining average is
+// removed in round r (O(log n / eps) rounds); rank = (round, degree, id).  Orienting by it
+// bounds |N+(u)| by the remaining degree at removal, <= 2(1 + eps) x the degeneracy.
+__global__ void k_adg_init(const int64_t* __restrict__ off, int64_t n, int32_t* __restrict__ dr,
+                           uint8_t* __restrict__ lvl) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        dr[v] = (int32_t)(off[v + 1] - off[v]);
+        lvl[v] = 0xff;
+    }
+}
+
+// sum of remaining degrees and remaining count ([0], [1])
+__global__ void k_adg_stats(const int32_t* __restrict__ dr, const uint8_t* __restrict__ lvl, int64_t n,
+                            unsigned long long* __restrict__ acc) {
+    unsigned long long sd = 0, c = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if (lvl[v] == 0xff) {
+            sd += (unsigned long long)max(dr[v], 0);
+            ++c;
+        }
+    for (int o = 16; o; o >>= 1) {
+        sd += __shfl_xor_sync(0xffffffffu, sd, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if ((threadIdx.x & 31) == 0 && c) {
+        atomicAdd(acc, sd);
+        atomicAdd(acc + 1, c);
+    }
+}
+
+// round r: remove the remaining vertices with dr <= thr (queued)
+__global__ void k_adg_mark(const int32_t* __restrict__ dr, uint8_t* __restrict__ lvl, int64_t n, int64_t thr, int r,
+                           int32_t* __restrict__ q, unsigned long long* __restrict__ qn) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if (lvl[v] == 0xff && (int64_t)dr[v] <= thr) {
+            lvl[v] = (uint8_t)r;
+            q[atomicAdd(qn, 1ull)] = (int32_t)v;
+        }
+}
+
+// warp per removed vertex: its still-remaining neighbours lose one remaining degree
+__global__ void k_adg_peel(const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                           const int32_t* __restrict__ q, int64_t qn, const uint8_t* __restrict__ lvl,
+                           int32_t* __restrict__ dr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < qn; t += nw) {
+        const int32_t v = q[t];
+        for (int64_t x = off[v] + lane; x < off[v + 1]; x += 32) {
+            const int32_t w = cols[x];
+            if (lvl[w] == 0xff) atomicSub(&dr[w], 1);
+        }
+    }
+}
+
+__global__ void k_adg_keys(const int64_t* __restrict__ off, const uint8_t* __restrict__ lvl, int64_t n,
+                           uint64_t* __restrict__ keys) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t dd = off[v + 1] - off[v];
+        const uint64_t d = (uint64_t)(dd < (1 << 24) - 1 ? dd : (1 << 24) - 1);
+        keys[v] = ((uint64_t)lvl[v] << 56) | (d << 32) | (uint64_t)v;
     }
 }
 
@@ -251,6 +318,44 @@ static int grid_for(int64_t items, int threads = 256) {
     if (b < 1) b = 1;
     if (b > 148 * 64) b = 148 * 64;
     return (int)b;
+}
+
+// keys = (peeling round, degree, id) of the approximate degeneracy order (k_adg_*)
+static void adg_keys(const int64_t* off, const int32_t* cols, int64_t n, int64_t nnz, uint64_t* keys, cudaStream_t s) {
+    (void)nnz;
+    DevBuf<int32_t> dr, q;
+    DevBuf<uint8_t> lvl;
+    DevBuf<unsigned long long> acc;
+    dr.ensure(n, s);
+    q.ensure(n, s);
+    lvl.ensure(n, s);
+    acc.ensure(3, s);
+    const unsigned gb = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    k_adg_init<<<gb, 256, 0, s>>>(off, n, dr.p, lvl.p);
+    GSM_LAUNCH("k_adg_init");
+    const double eps = 0.25;
+    for (int r = 0; r < 254; ++r) {
+        GSM_CUDA(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), s));
+        k_adg_stats<<<gb, 256, 0, s>>>(dr.p, lvl.p, n, acc.p);
+        GSM_LAUNCH("k_adg_stats");
+        unsigned long long h[2];
+        GSM_CUDA(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        if (h[1] == 0) break;
+        // the last admissible round takes everything left
+        const int64_t thr = r == 253 ? INT64_MAX : (int64_t)((1.0 + eps) * (double)h[0] / (double)h[1]);
+        k_adg_mark<<<gb, 256, 0, s>>>(dr.p, lvl.p, n, thr, r, q.p, acc.p + 2);
+        GSM_LAUNCH("k_adg_mark");
+        unsigned long long qn = 0;
+        GSM_CUDA(cudaMemcpyAsync(&qn, acc.p + 2, sizeof(qn), cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        if (qn == h[1]) break;  // nothing remains to update
+        k_adg_peel<<<(unsigned)std::min<int64_t>((qn + 7) / 8, 148 * 64), 256, 0, s>>>(off, cols, q.p, (int64_t)qn,
+                                                                                     lvl.p, dr.p);
+        GSM_LAUNCH("k_adg_peel");
+    }
+    k_adg_keys<<<gb, 256, 0, s>>>(off, lvl.p, n, keys);
+    GSM_LAUNCH("k_adg_keys");
 }
 
 static int bits_for(uint64_t x) {
@@ -367,7 +472,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
     g.new2old = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
     g.old2new = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
 
-    // 1. rank by (degree, id)
+    // 1. rank by (degree, id) (GSM_ORDER=1: by (peeling round, degree, id), k_adg_*)
     {
         DevBuf<uint64_t> keys, sorted;
         DevBuf<int> maxdeg;
@@ -381,7 +486,11 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         GSM_CUDA(cudaMemcpyAsync(&hmax, maxdeg.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         GSM_CUDA(cudaStreamSynchronize(s));
         g.max_degree = hmax;
-        const int end_bit = 32 + bits_for((uint64_t)hmax);
+        int end_bit = 32 + bits_for((uint64_t)hmax);
+        if (knobs().order == 1 && n > 1) {
+            end_bit = 64;
+            adg_keys(d_off, d_cols, n, nnz, keys.p, s);
+        }
         size_t tmp_bytes = 0;
         GSM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, sorted.p, n, 0, end_bit, s));
         DevBuf<uint8_t> tmp;
@@ -389,7 +498,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         GSM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, n, 0, end_bit, s));
         DevBuf<int64_t> newdeg;
         newdeg.ensure(n, s);
-        k_permutation<<<grid_for(n), 256, 0, s>>>(sorted.p, n, g.new2old, g.old2new, newdeg.p);
+        k_permutation<<<grid_for(n), 256, 0, s>>>(sorted.p, d_off, n, g.new2old, g.old2new, newdeg.p);
         GSM_LAUNCH("k_permutation");
         GSM_CUDA(cudaMemsetAsync(g.off, 0, sizeof(int64_t), s));
         size_t sb = 0;

@@ -224,6 +224,25 @@ def test_config4_rmat24_cliques_exact(rmat24, k):
         assert cv == want, ("root", v, cv, want)
 
 
+def test_config4_rmat24_cliques_degeneracy_order(rmat24, monkeypatch):
+    """GSM_ORDER=1 (approximate degeneracy rank, another valid ≺): K3 and K4 totals at full
+    scale still equal the oracle's independent counter (golden file)."""
+    w, g, _ = rmat24
+    gold = _golden24()
+    monkeypatch.setenv("GSM_ORDER", "1")
+    G = load(g, validate=False)
+    monkeypatch.delenv("GSM_ORDER")
+    try:
+        for k, fact in ((3, 6), (4, 24)):
+            if f"K{k}" not in gold:
+                continue
+            c, _, r = run(G, gi.query(f"K{k}"), "count", mem_budget_bytes=w.mem_budget_bytes)
+            assert r.prof["clique"]["launches"] > 0
+            assert c == fact * gold[f"K{k}"]["total"], (k, c)
+    finally:
+        G.free()
+
+
 def test_config4_rmat24_k4_chunked_bfs_and_samples(rmat24, monkeypatch):
     """The north_star's breadth-first path (GSM_CLIQUE=0: chunked frontier under the fixed
     16 GiB budget) on the same graph, and root-sampled sorted-row parity vs the DFS oracle."""

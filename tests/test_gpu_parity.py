@@ -402,7 +402,8 @@ def test_compressed_partials(variant, monkeypatch):
     G = load(g)
     try:
         qs = [gi.query("house"), gi.query("K4"), gi.query("P4", [0, 1, 1, 0]), gi.query("C5"),
-              gi.Query(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (0, 3)], None, "C6+chord"),
+              # labeled: the unlabeled C6+chord has 1.7e9 embeddings here (40 GB of rows, ~550 s per variant)
+              gi.Query(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (0, 3)], [0, 1, 0, 1, 0, 1], "C6+chord"),
               gi.random_connected_query(6, 2, 77, 2)]
         for q in qs:
             cnt, ref = oracle.match(g, q)
@@ -622,5 +623,36 @@ def test_device_pointer_load_and_profile():
         assert t.is_cuda and t.shape[0] == c
         assert np.array_equal(t.cpu().numpy(), rt)
         re.free()
+    finally:
+        G.free()
+
+
+@pytest.mark.parametrize("hub", ["hub", "nohub"])
+def test_degeneracy_order(hub, dense_gnp, monkeypatch):
+    """GSM_ORDER=1 (read at gsm_load_graph): data vertices ranked by an approximate
+    degeneracy (peeling-round) order instead of (degree, id).  Any strict total order is a
+    valid ≺ (SURVEY §8(c) amb. 9): every mode's rows equal the oracle's, the clique kernels'
+    counts equal the independent clique counters."""
+    monkeypatch.setenv("GSM_ORDER", "1")
+    if hub == "nohub":
+        monkeypatch.setenv("GSM_HUB_BITS", "0")
+    g = gi.rmat(10, 16, seed=12)
+    G = load(g)
+    try:
+        for qn in ["K3", "K4", "C4", "P4", "house"]:
+            check_all_modes(g, gi.query(qn), G, f"order1 {qn}")
+    finally:
+        G.free()
+    h = gi.rmat(11, 8, seed=3).with_labels(gi.uniform_labels(2048, 3, 3))
+    H = load(h)
+    try:
+        check_all_modes(h, gi.query("house", [0, 1, 2, 0, 1]), H, "order1 labeled house")
+    finally:
+        H.free()
+    gd, T, K4 = dense_gnp
+    G = load(gd)
+    try:
+        assert run(G, gi.query("K3"), "count", flags=gsm.GSM_FLAG_UNIQUE)[0] == T
+        assert run(G, gi.query("K4"), "count", flags=gsm.GSM_FLAG_UNIQUE)[0] == K4
     finally:
         G.free()

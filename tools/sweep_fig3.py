@@ -1,14 +1,26 @@
-"""Fig.-3-shaped sweeps on synthetic graphs (PAPER P:218-220:
-random-walk queries of a given size, power-law labels; Fig. 3 varies query size and
-label count).  Not a bench line: each point prints one JSON line with the CUDA path's
-device time (CUDA events on the match stream, median of --reps after one warm-up) and
-its count, checked against the oracle's count (test infrastructure, P:70 definition).
+"""Fig.-3-shaped sweeps on synthetic graphs (PAPER P:213-220:
+"size from 3 vertices to 13 vertices" (Fig. 3 left) and "10 different queries with
+12 nodes and 22 edges" on "power-law-distributed node ... labels" from 20 to 200,
+each query run 10 times, mean runtime (Fig. 3 right)).  Not a bench line: each point
+prints one JSON line with the CUDA path's device time (CUDA events on the match stream,
+one warm-up, then mean and median of --reps runs) and its count, checked against the
+oracle (test infrastructure, the P:70 definition):
 
-    python tools/sweep_fig3.py --scale 13 --out gpurun_out/fig3_sweep.jsonl
+  * full count when the plain DFS finishes within --oracle-s (forked, killed after);
+  * otherwise root-sampled parity: all embeddings with f(query vertex 0) in a fixed
+    strided sample of --sample-roots vertices, on both sides (GSM root_subset).
+
+Graphs: Enron-shaped R-MAT (scale 15, edge factor 8: 32k vertices, ~5 avg degree like
+Enron's 36.7k / 183.8k) for the query-size axis, Gowalla-shaped R-MAT (scale 17,
+edge factor 8: 131k vertices, Gowalla 196.6k / 950.3k) for the label axis.
+
+    python tools/sweep_fig3.py --out gpurun_out/fig3_sweep.jsonl
 """
 import argparse
 import json
+import multiprocessing as mp
 import os
+import statistics
 import sys
 import time
 
@@ -21,60 +33,108 @@ import oracle  # noqa: E402
 from paper_2003_01527_b200 import gsm  # noqa: E402
 
 
-def time_match(G, q, reps):
+def time_match(G, q, reps, root_subset=None):
     s = torch.cuda.Stream()
     ts, cnt = [], None
     for i in range(reps + 1):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record(s)
-        r = gsm.gsm_match(G, q.num_nodes, q.edges, q.labels, mode=gsm.GSM_MODE_COUNT, stream=s.cuda_stream)
+        r = gsm.gsm_match(G, q.num_nodes, q.edges, q.labels, mode=gsm.GSM_MODE_COUNT, stream=s.cuda_stream,
+                          root_subset=root_subset)
         b.record(s)
         torch.cuda.synchronize()
         cnt = r.count
         r.free()
         if i:
             ts.append(a.elapsed_time(b))
-    return cnt, float(np.median(ts))
+    return cnt, statistics.mean(ts), statistics.median(ts)
 
 
-def point(out, g, G, q, sweep, x, reps):
-    c, ms = time_match(G, q, reps)
+def _child(conn, g, q, roots):
     t0 = time.perf_counter()
-    ref, _ = oracle.match(g, q, count_only=True)
-    ot = time.perf_counter() - t0
-    rec = {"sweep": sweep, "x": x, "query": q.name, "k": q.num_nodes, "edges": len(q.edges),
-           "count": c, "oracle_count": ref, "match": c == ref, "gpu_ms": ms,
-           "oracle_s": ot, "oracle_threads": oracle.num_threads()}
+    c = oracle.match(g, q, roots=roots, count_only=True)[0]
+    conn.send((c, time.perf_counter() - t0))
+    conn.close()
+
+
+def oracle_bounded(g, q, roots, limit_s):
+    ctx = mp.get_context("fork")
+    a, b = ctx.Pipe(duplex=False)
+    p = ctx.Process(target=_child, args=(b, g, q, roots), daemon=True)
+    p.start()
+    b.close()
+    res = a.recv() if a.poll(limit_s) else None
+    if p.is_alive():
+        p.kill()
+    p.join()
+    return res
+
+
+def point(out, g, G, q, sweep, x, args):
+    c, ms_mean, ms_med = time_match(G, q, args.reps)
+    rec = {"sweep": sweep, "x": x, "graph": g.name, "query": q.name, "k": q.num_nodes, "edges": len(q.edges),
+           "count": c, "gpu_ms_mean": ms_mean, "gpu_ms_median": ms_med, "oracle_threads": oracle.num_threads()}
+    res = oracle_bounded(g, q, None, args.oracle_s)
+    if res is not None:
+        rec.update(parity="full", oracle_count=res[0], oracle_s=res[1], match=c == res[0])
+    else:
+        n = g.num_nodes
+        cnt = min(n, args.sample_roots)
+        roots = np.unique((np.arange(cnt) * (n / cnt)).astype(np.int64)).astype(np.int32)
+        cs, _, _ = time_match(G, q, 0, root_subset=roots)
+        res = oracle_bounded(g, q, roots, 4 * args.oracle_s)
+        if res is None:
+            rec.update(parity="none (oracle sample over time limit)", match=None)
+        else:
+            rec.update(parity=f"root-sampled ({len(roots)} strided roots)", sample_count=cs, oracle_count=res[0],
+                       oracle_s=res[1], match=cs == res[0])
     print(json.dumps(rec), flush=True)
     out.write(json.dumps(rec) + "\n")
     out.flush()
-    return c == ref
+    return rec["match"] is not False
 
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--scale", type=int, default=13)
-    p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--reps", type=int, default=10)
+    p.add_argument("--oracle-s", type=float, default=20.0)
+    p.add_argument("--sample-roots", type=int, default=512)
+    p.add_argument("--queries", type=int, default=10, help="random-walk queries per label count (P:220)")
     p.add_argument("--out", default="gpurun_out/fig3_sweep.jsonl")
     a = p.parse_args()
     ok = True
-    base = gi.rmat(a.scale, 16, 1)
     with open(a.out, "w") as out:
-        # (a) query size 3..7 with 20 Zipf labels; 2k-3 edges.  Larger or sparser
-        # queries make the plain-DFS oracle's counts (and time) explode on Zipf labels.
+        # (a) query size 3..13, 20 Zipf labels, random-walk queries with 2k-3 edges
+        # (a tree plus k-2 non-tree edges when the walk's induced subgraph has them)
+        base = gi.rmat(15, 8, 1)
         g = base.with_labels(gi.zipf_labels(base.num_nodes, 20, 1), tag="-Z20")
         G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=0)
-        for k in range(3, 8):
-            q = gi.random_walk_query(g, k, max(3, 2 * k - 3), seed=1000 + k)
-            ok &= point(out, g, G, q, "query_size", k, a.reps)
+        for k in range(3, 14):
+            q = None
+            for e in range(2 * k - 3, k - 2, -1):  # as dense as the walks allow
+                try:
+                    q = gi.random_walk_query(g, k, max(k - 1, e), seed=1000 + k)
+                    break
+                except RuntimeError:
+                    continue
+            ok &= point(out, g, G, q, "query_size", k, a)
         G.free()
-        # (b) label count 20..200 at query size 6 (Fig. 3 label axis)
-        for L in (20, 50, 100, 200):
+        # (b) label count 20..200: 10 random-walk queries of 12 nodes / 22 edges each
+        base = gi.rmat(17, 8, 1)
+        for L in (20, 50, 100, 150, 200):
             g = base.with_labels(gi.zipf_labels(base.num_nodes, L, 1), tag=f"-Z{L}")
             G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=0)
-            q = gi.random_walk_query(g, 6, 9, seed=2000 + L)
-            ok &= point(out, g, G, q, "labels", L, a.reps)
+            made = 0
+            for s in range(200):
+                if made == a.queries:
+                    break
+                try:
+                    q = gi.random_walk_query(g, 12, 22, seed=2000 + 97 * L + s)
+                except RuntimeError:
+                    continue
+                made += 1
+                ok &= point(out, g, G, q, "labels", L, a)
             G.free()
     print("ALL MATCH" if ok else "MISMATCH", flush=True)
     sys.exit(0 if ok else 1)

@@ -267,6 +267,19 @@ GSM_API gsm_status gsm_sort_rows(int32_t* rows, uint64_t num_rows, int32_t width
                                  void* stream);
 
 /*
+ * gsm_merge_rows — merge two lexicographically sorted (unsigned tuple) row blocks
+ * a (na x width) and b (nb x width) into out ((na + nb) x width), all int32 in DEVICE memory
+ * on `device`; out must not overlap a or b.  The P-way merge of the locally sorted ENUMERATE
+ * shards of P GPUs ("a P-way merge of the locally pre-sorted
+ * shards") is a tree of these.  Equal rows keep a's first.  Merge-path partition: each thread
+ * binary-searches its output diagonal, then merges 8 rows.  Synchronous on `stream` (NULL =
+ * legacy default stream).  Errors: GSM_ERR_INVALID_ARGUMENT (null pointer with a non-zero
+ * count, width outside 1..32), GSM_ERR_CUDA.
+ */
+GSM_API gsm_status gsm_merge_rows(const int32_t* a, uint64_t na, const int32_t* b, uint64_t nb, int32_t width,
+                                  int32_t* out, int32_t device, void* stream);
+
+/*
  * gsm_filter_candidates — the candidate filter alone (Alg. 1 lines 6-9, PAPER P:108-110,
  * P:129): out[v] for every data vertex v (ORIGINAL id order) = bitmask of the query
  * vertices u with v in C(u): label(v) = label_Q(u) and deg(v) >= deg_Q(u), then

@@ -82,7 +82,8 @@ class gsm_plan_info(ctypes.Structure):
 _lib = None
 
 EXPORTS = ["gsm_load_graph", "gsm_free", "gsm_graph_info", "gsm_match", "gsm_result_free", "gsm_result_copy_rows",
-           "gsm_plan_query", "gsm_sort_rows", "gsm_filter_candidates", "gsm_last_error", "gsm_version"]
+           "gsm_plan_query", "gsm_sort_rows", "gsm_merge_rows", "gsm_filter_candidates", "gsm_last_error",
+           "gsm_version"]
 
 
 def lib():
@@ -102,6 +103,7 @@ def lib():
         L.gsm_result_copy_rows.argtypes = [ctypes.POINTER(gsm_result), P, i32]
         L.gsm_plan_query.argtypes = [ctypes.POINTER(gsm_query), P, ctypes.c_uint32, ctypes.POINTER(gsm_plan_info)]
         L.gsm_sort_rows.argtypes = [P, ctypes.c_uint64, i32, i64, i32, P]
+        L.gsm_merge_rows.argtypes = [P, ctypes.c_uint64, P, ctypes.c_uint64, i32, P, i32, P]
         L.gsm_filter_candidates.argtypes = [P, ctypes.POINTER(gsm_query), i32, P, i32]
         L.gsm_last_error.restype = ctypes.c_char_p
         L.gsm_version.restype = ctypes.c_char_p
@@ -288,6 +290,21 @@ def gsm_sort_rows(rows, max_id: int, stream: Optional[int] = None):
     _check(lib().gsm_sort_rows(ctypes.c_void_p(rows.data_ptr()), rows.shape[0], rows.shape[1], int(max_id),
                                rows.device.index or 0, stream))
     return rows
+
+
+def gsm_merge_rows(a, b, stream: Optional[int] = None):
+    """Merge two lexicographically sorted CUDA int32 row tensors (na x w, nb x w) on the same
+    device into a new (na + nb) x w tensor (the library's merge-path kernel)."""
+    import torch
+    for name, t in (("a", a), ("b", b)):
+        if not (hasattr(t, "is_cuda") and t.is_cuda and t.is_contiguous() and t.dim() == 2 and t.dtype == torch.int32):
+            raise ValueError(f"gsm_merge_rows: {name} must be a contiguous 2-D CUDA int32 tensor")
+    if a.shape[1] != b.shape[1] or a.device != b.device:
+        raise ValueError("gsm_merge_rows: a and b need the same width and device")
+    out = torch.empty((a.shape[0] + b.shape[0], a.shape[1]), dtype=torch.int32, device=a.device)
+    _check(lib().gsm_merge_rows(ctypes.c_void_p(a.data_ptr()), a.shape[0], ctypes.c_void_p(b.data_ptr()), b.shape[0],
+                                a.shape[1], ctypes.c_void_p(out.data_ptr()), a.device.index or 0, stream))
+    return out
 
 
 def gsm_filter_candidates(g: Graph, num_nodes: int, edges: Sequence, labels=None, refine_rounds: int = 0):

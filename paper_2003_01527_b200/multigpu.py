@@ -6,9 +6,12 @@ each rank keeps the roots whose (degree, id) rank r satisfies r % P == rank
 (hubs spread round-robin), runs the whole hot path on them with no exchange,
 and the ranks meet once at the end:
   * COUNT      — one all-reduce of the uint64 counts (16 B);
-  * ENUMERATE  — all-gather of the per-rank row counts, all-gather of the rows
-                 padded to the largest shard, then one lexicographic sort of
-                 the concatenation (gsm_sort_rows, the library's radix sort).
+  * ENUMERATE  — all-gather of the per-rank row counts, then every rank's
+                 exact-size row block by one broadcast per source rank (an
+                 all-gather-v: no padding to the largest shard), then a tree
+                 of pairwise merges of the locally sorted shards
+                 (gsm_merge_rows, the library's merge-path kernel): log2 P
+                 rounds, no re-sort of the concatenation.
 torch.distributed is the plumbing (NCCL over NVLink on GPUs; gloo in the CPU
 tests of the collective logic); the matching itself is libgsm's kernels.
 """
@@ -33,30 +36,54 @@ def allreduce_counts(values: Sequence[int], dist, device) -> list:
     return [int(x) for x in t.tolist()]
 
 
-def allgather_rows(rows, dist):
-    """All-gather variable-length row blocks (N_r x k int32 tensors) -> concatenation in rank order."""
+def gather_row_blocks(rows, dist) -> list:
+    """All-gather-v of variable-length row blocks (N_r x k int32 tensors): the per-rank counts
+    first, then each rank's block at its exact size by a broadcast from that rank.  Returns
+    the list of blocks in rank order (this rank's own block is ``rows`` itself)."""
     import torch
     if _host_collectives(dist) and rows.is_cuda:
-        return allgather_rows(rows.cpu(), dist).to(rows.device)
-    world = dist.get_world_size()
+        return [b.to(rows.device) for b in gather_row_blocks(rows.cpu(), dist)]
+    world, me = dist.get_world_size(), dist.get_rank()
     k = rows.shape[1]
     n = torch.tensor([rows.shape[0]], dtype=torch.int64, device=rows.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n)
-    sizes = [int(s.item()) for s in sizes]
-    mx = max(sizes)
-    if mx == 0:
-        return rows.new_zeros((0, k))
-    padded = rows.new_zeros((mx, k))
-    padded[: rows.shape[0]] = rows
-    bufs = [rows.new_zeros((mx, k)) for _ in range(world)]
-    dist.all_gather(bufs, padded)
-    return torch.cat([b[:s] for b, s in zip(bufs, sizes)], dim=0)
+    sizes = [int(x.item()) for x in sizes]
+    blocks = []
+    for r in range(world):
+        if sizes[r] == 0:
+            blocks.append(rows.new_zeros((0, k)))
+            continue
+        buf = rows.contiguous() if r == me else rows.new_empty((sizes[r], k))
+        dist.broadcast(buf, src=r)
+        blocks.append(buf)
+    return blocks
+
+
+def merge_sorted_blocks(blocks: list, merge_fn: Callable):
+    """Tree of pairwise merges of lexicographically sorted row blocks (ceil(log2 P) rounds)."""
+    blocks = [b for b in blocks if b.shape[0] > 0] or blocks[:1]
+    while len(blocks) > 1:
+        nxt = [merge_fn(blocks[i], blocks[i + 1]) for i in range(0, len(blocks) - 1, 2)]
+        if len(blocks) % 2:
+            nxt.append(blocks[-1])
+        blocks = nxt
+    return blocks[0]
+
+
+def allgather_rows(rows, dist, merge_fn: Optional[Callable] = None):
+    """All sorted row blocks of every rank merged into one sorted block (on every rank)."""
+    blocks = gather_row_blocks(rows, dist)
+    if merge_fn is None:
+        if not rows.is_cuda:
+            raise ValueError("allgather_rows: host row blocks need an explicit merge_fn (the library merges on the GPU)")
+        merge_fn = gsm.gsm_merge_rows
+    return merge_sorted_blocks(blocks, merge_fn)
 
 
 def match_sharded(G: "gsm.Graph", num_nodes: int, edges, labels=None, mode: int = gsm.GSM_MODE_COUNT, flags: int = 0,
                   dist=None, num_graph_nodes: Optional[int] = None, mem_budget_bytes: int = 0,
-                  stream: Optional[int] = None, sort_fn: Optional[Callable] = None):
+                  stream: Optional[int] = None, merge_fn: Optional[Callable] = None):
     """Run gsm_match on this rank's root shard and combine across ranks.
     Returns (count, count_unique, rows or None); rows (ENUMERATE) are the full,
     sorted embedding list on every rank."""
@@ -72,11 +99,11 @@ def match_sharded(G: "gsm.Graph", num_nodes: int, edges, labels=None, mode: int 
             count, count_unique = allreduce_counts([count, count_unique], dist, dev)
         rows = None
         if mode == gsm.GSM_MODE_ENUMERATE:
-            local = r.rows_torch(dev)
-            rows = allgather_rows(local, dist) if dist is not None else local
-            if world > 1 and rows.shape[0]:
-                n = num_graph_nodes if num_graph_nodes is not None else int(rows.max().item()) + 1
-                (sort_fn or (lambda t: gsm.gsm_sort_rows(t, n - 1, stream)))(rows)
+            local = r.rows_torch(dev)  # sorted by gsm_match
+            if dist is not None and world > 1:
+                rows = allgather_rows(local, dist, merge_fn)
+            else:
+                rows = local
         return count, count_unique, rows
     finally:
         r.free()

@@ -656,3 +656,19 @@ def test_degeneracy_order(hub, dense_gnp, monkeypatch):
         assert run(G, gi.query("K4"), "count", flags=gsm.GSM_FLAG_UNIQUE)[0] == K4
     finally:
         G.free()
+
+
+def test_merge_rows():
+    """gsm_merge_rows (merge path): two sorted row blocks -> the sorted
+    concatenation, element by element against oracle.sort_rows; empty sides, ragged sizes,
+    equal rows across the blocks, widths 1..5."""
+    import torch
+    rng = np.random.default_rng(17)
+    for w, na, nb, hi in [(1, 0, 5, 9), (3, 7, 0, 9), (2, 1000, 3, 4), (3, 12345, 54321, 50), (5, 200000, 150001, 1 << 24),
+                          (4, 1, 1, 2)]:
+        a = oracle.sort_rows(rng.integers(0, hi, size=(na, w)).astype(np.int32))
+        b = oracle.sort_rows(rng.integers(0, hi, size=(nb, w)).astype(np.int32))
+        ta = torch.from_numpy(a).cuda().reshape(na, w)
+        tb = torch.from_numpy(b).cuda().reshape(nb, w)
+        out = gsm.gsm_merge_rows(ta, tb).cpu().numpy()
+        assert_rows_equal(out, oracle.sort_rows(np.concatenate([a, b]).reshape(-1, w)), f"merge w={w} {na}+{nb}")

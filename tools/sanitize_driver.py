@@ -25,6 +25,11 @@ def main():
     for q in (gi.query("K3"), gi.query("K4")):
         print(q.name, m(G, q))
     G.free()
+    os.environ["GSM_ORDER"] = "1"  # approximate degeneracy order (k_adg_* at load)
+    G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, None)
+    print("K4 order1", m(G, gi.query("K4")))
+    G.free()
+    del os.environ["GSM_ORDER"]
     os.environ["GSM_HUB_BITS"] = "0"
     os.environ["GSM_CLIQUE_DSMEM"] = "64"  # global-slab kernel
     G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, None)

@@ -636,7 +636,7 @@ def test_degeneracy_order(hub, dense_gnp, monkeypatch):
     monkeypatch.setenv("GSM_ORDER", "1")
     if hub == "nohub":
         monkeypatch.setenv("GSM_HUB_BITS", "0")
-    g = gi.rmat(10, 16, seed=12)
+    g = gi.rmat(9, 8, seed=12)  # house: 4.3e7 rows (R-MAT-10 ef16: 1.5e9 — 20 min per variant)
     G = load(g)
     try:
         for qn in ["K3", "K4", "C4", "P4", "house"]:

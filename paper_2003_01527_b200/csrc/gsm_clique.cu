@@ -145,6 +145,9 @@ struct CliqueArgs {
     int32_t hub_base;       // first hub rank
     int32_t hub_words;      // H / 32
     int32_t hub_ratio;      // k_clique_cta: a hub row takes bitmap lookups when 32 nj <= hub_ratio |N+(a)|
+    const int32_t* nh_off;  // hashed N+(v) tables (DevGraph::nh_*) or nullptr
+    const int32_t* nh_tab;
+    int32_t nh_stream;      // with a table, a row streams N+(S[i]) only when 32 |N+(S[i])| <= nh_stream x nj
     int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
     unsigned long long* next;   // dynamic root scheduler
     unsigned long long* count;  // unique cliques (atomic)
@@ -186,6 +189,13 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
                     const int c = sv - a.hub_base;
                     f = (__ldg(hr + (c >> 5)) >> (c & 31)) & 1u;
                 }
+                bits = __ballot_sync(kFull, f);
+                items += live;
+            } else if (a.nh_off && 32 * (le - ls) > (int64_t)a.nh_stream * nj && __ldg(a.nh_off + ai) >= 0) {
+                // hashed N+(S[i]): one bucket (32-byte sector) per remaining S[j]
+                const int32_t tb = __ldg(a.nh_off + ai);
+                const bool live = lane > i && lane < d;
+                const bool f = live && nh_find(a.nh_tab, tb, nh_buckets(le - ls), sv, probes);
                 bits = __ballot_sync(kFull, f);
                 items += live;
             } else if (le - ls <= (int64_t)a.stream_max) {
@@ -422,6 +432,30 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                         f = (__ldg(hr + (c >> 5)) >> (c & 31)) & 1u;
                     }
                     items += live;
+                    const unsigned bits = __ballot_sync(kFull, f);
+                    if (K == 4) {
+                        if (lane == 0) Ai[w] = bits;
+                    } else {
+                        cnt += f;
+                    }
+                }
+                if (a.cyc) {
+                    const long long t1 = clock64();
+                    cy[2] += t1 - tc;
+                    tc = t1;
+                }
+                continue;
+            }
+            // hashed N+(S[i]) (load-time table): one 32-byte bucket per remaining S[j], unless
+            // streaming the list is cheaper (32 len <= nh_stream x nj)
+            const int32_t tb = a.nh_off ? __ldg(a.nh_off + ai) : -1;
+            if (tb >= 0 && !(use_ck && (int64_t)len * 32 <= (int64_t)a.nh_stream * nj)) {
+                const unsigned B = nh_buckets(len);
+                for (int w = w0; w < W; ++w) {
+                    const int j = (w << 5) + lane;
+                    const bool live = j > i && j < d;
+                    items += live;
+                    const bool f = live && nh_find(a.nh_tab, tb, B, S[j], probes);
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
                         if (lane == 0) Ai[w] = bits;
@@ -700,6 +734,9 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     a.hub_base = r.hub_base;
     a.hub_words = r.hub_words;
     a.hub_ratio = knobs().clique_hub_ratio;
+    a.nh_off = r.nh_off;
+    a.nh_tab = r.nh_tab;
+    a.nh_stream = knobs().clique_nh_stream;
     DevBuf<unsigned long long> cyc;
     a.cyc = nullptr;
     if (knobs().trace == 2) {

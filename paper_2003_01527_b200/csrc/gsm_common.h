@@ -39,7 +39,43 @@ struct DevGraph {
     int32_t hub_base = 0;
     int32_t hub_words = 0;        // H / 32
     int64_t hub_bytes = 0;
+    // Hashed N+(v) ("membership tables"): for every v with |N+(v)| >= nh_min, an
+    // open-addressing table of N+(v) in 32-byte buckets of 8 int32 slots (one DRAM sector;
+    // nh_buckets(|N+(v)|) buckets, load <= 1/2, -1 = empty, slots filled from slot 0, overflow
+    // to the next bucket).  nh_off[v] = first bucket of v's table, or -1.  A membership test
+    // x ∈ N+(v) is then one sector load (rarely two) instead of a binary search over
+    // log2 |N+(v)| dependent probes.  nullptr = disabled (GSM_NHASH_MIN=0).
+    int32_t* nh_off = nullptr;
+    int32_t* nh_tab = nullptr;
+    int64_t nh_buckets_total = 0;
+    int32_t nh_min = 0;
 };
+
+// buckets of the N+(v) table of a list of length L (a power of two >= L / 4)
+__host__ __device__ __forceinline__ unsigned nh_buckets(int64_t L) {
+    unsigned b = 1;
+    while ((int64_t)b * 4 < L) b <<= 1;
+    return b;
+}
+__host__ __device__ __forceinline__ unsigned nh_hash(int32_t x, unsigned B) {
+    return ((unsigned)x * 0x9E3779B1u) & (B - 1);  // B is a power of two
+}
+#ifdef __CUDACC__
+// x ∈ N+(v), given v's table (first bucket tb) of B buckets: one 32-byte bucket per probe
+__device__ __forceinline__ bool nh_find(const int32_t* __restrict__ tab, int32_t tb, unsigned B, int32_t x,
+                                        unsigned& probes) {
+    unsigned b = nh_hash(x, B);
+    for (;;) {
+        const int4* p = reinterpret_cast<const int4*>(tab + 8 * ((int64_t)tb + b));
+        const int4 u = __ldg(p), w = __ldg(p + 1);
+        ++probes;
+        if ((u.x == x) | (u.y == x) | (u.z == x) | (u.w == x) | (w.x == x) | (w.y == x) | (w.z == x) | (w.w == x))
+            return true;
+        if (w.w < 0) return false;  // bucket not full: x would have been placed here
+        b = (b + 1) & (B - 1);
+    }
+}
+#endif
 
 // pointer p with p[c >> 5] = the word holding column c (c > r) of hub row r
 __host__ __device__ __forceinline__ const uint32_t* hub_row(const uint32_t* bits, int hw, int r) {
@@ -105,13 +141,15 @@ struct Knobs {
     int expand_ilp = 1;       // GSM_EXPAND_ILP (1, 2 or 4)
     int trace = 0;            // GSM_TRACE: 1 host trace, 2 per-phase cycle counters
     int member_hub = 1;       // GSM_MEMBER_HUB: pair-tail membership tests of two hubs by the hub bitmap
-    int member_swap = 64;     // GSM_MEMBER_SWAP: segments longer than this may search in N(v) (0 = never)
-    int plan_groups = 1;      // GSM_PLAN_GROUPS: row plans by lane groups (one lane per backward neighbour)
+    int member_swap = 0;      // GSM_MEMBER_SWAP: segments longer than this may search in N(v) (0 = never; R-MAT-22 284 vs 136 ms)
+    int plan_groups = 0;      // GSM_PLAN_GROUPS: row plans by lane groups (R-MAT-22 plan 19.6 vs 15.5 ms: off)
     int compress = -1;        // GSM_COMPRESS: 1/0 force the compressed partial layout on/off (-1 = flag)
     int lookahead = -1;       // GSM_LOOKAHEAD: overrides gsm_match_opts.lookahead when >= 0
     int hub_bits = 32768;     // GSM_HUB_BITS: H of the hub adjacency bitmap built at load (0 = none)
     int clique_hub = 1;       // GSM_CLIQUE_HUB: clique rows of a hub pivot by bitmap lookups
     int clique_hub_ratio = 64;  // GSM_CLIQUE_HUB_RATIO: lookups when 32 nj <= ratio |N+(S[i])|
+    int nhash_min = 16;       // GSM_NHASH_MIN (read at gsm_load_graph): hashed N+(v) for |N+(v)| >= this (0 = none)
+    int clique_nh_stream = 64;  // GSM_CLIQUE_NH_STREAM: with a table, stream N+(S[i]) when 32 len <= this x nj
     int order = 0;            // GSM_ORDER (read at gsm_load_graph): 0 = rank by (degree, id), 1 = approximate degeneracy
 };
 void load_knobs();

@@ -77,6 +77,8 @@ void load_knobs() {
     k.clique_hub = env_or("GSM_CLIQUE_HUB", k.clique_hub);
     k.clique_hub_ratio = env_or("GSM_CLIQUE_HUB_RATIO", k.clique_hub_ratio);
     k.order = env_or("GSM_ORDER", k.order);
+    k.nhash_min = std::max(0, env_or("GSM_NHASH_MIN", k.nhash_min));
+    k.clique_nh_stream = env_or("GSM_CLIQUE_NH_STREAM", k.clique_nh_stream);
     g_knobs = k;
 }
 
@@ -320,6 +322,49 @@ static int grid_for(int64_t items, int threads = 256) {
     return (int)b;
 }
 
+// ---------------------------------------------------------------- hashed N+(v) tables
+// buckets per vertex (0 when |N+(v)| < nh_min)
+__global__ void k_nh_sizes(const int64_t* __restrict__ off, const int32_t* __restrict__ up, int64_t n, int nh_min,
+                           int64_t* __restrict__ nb) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t L = off[v + 1] - off[v] - up[v];
+        nb[v] = L >= nh_min ? (int64_t)nh_buckets(L) : 0;
+    }
+}
+
+__global__ void k_nh_offsets(const int64_t* __restrict__ nb, const int64_t* __restrict__ excl, int64_t n,
+                             int32_t* __restrict__ nh_off) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        nh_off[v] = nb[v] ? (int32_t)excl[v] : -1;
+}
+
+// warp per vertex: insert every entry of N+(v) into v's table (first free slot of its bucket,
+// else the next bucket); the entries of one list are distinct, so no duplicate checks
+__global__ void k_nh_insert(const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                            const int32_t* __restrict__ up, const int32_t* __restrict__ nh_off, int64_t n,
+                            int32_t* __restrict__ tab) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += nw) {
+        const int32_t tb = nh_off[v];
+        if (tb < 0) continue;
+        const int64_t b0 = off[v] + up[v], e = off[v + 1];
+        const unsigned B = nh_buckets(e - b0);
+        for (int64_t x = b0 + lane; x < e; x += 32) {
+            const int32_t key = cols[x];
+            unsigned b = nh_hash(key, B);
+            for (bool done = false; !done; b = (b + 1) & (B - 1)) {
+                int32_t* slot = tab + 8 * ((int64_t)tb + b);
+                for (int q = 0; q < 8; ++q)
+                    if (atomicCAS(slot + q, -1, key) == -1) {
+                        done = true;
+                        break;
+                    }
+            }
+        }
+    }
+}
+
 // keys = (peeling round, degree, id) of the approximate degeneracy order (k_adg_*)
 static void adg_keys(const int64_t* off, const int32_t* cols, int64_t n, int64_t nnz, uint64_t* keys, cudaStream_t s) {
     (void)nnz;
@@ -375,7 +420,7 @@ static void free_graph(gsm_graph* h) {
     // graph arrays come from the device's stream-ordered pool (kept cached by its release
     // threshold, so a load/free/load cycle does not re-map memory)
     for (void* p : {(void*)g.off, (void*)g.cols, (void*)g.up, (void*)g.labels, (void*)g.lkeys, (void*)g.new2old,
-                    (void*)g.old2new, (void*)g.hub_bits})
+                    (void*)g.old2new, (void*)g.hub_bits, (void*)g.nh_off, (void*)g.nh_tab})
         if (p) cudaFreeAsync(p, h->stream);
     cudaStreamSynchronize(h->stream);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -548,6 +593,34 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
             k_hub_bits<<<grid_for((int64_t)H * 32), 256, 0, s>>>(g.off, g.cols, g.up, g.hub_base, H, g.hub_words,
                                                                  g.hub_bits);
             GSM_LAUNCH("k_hub_bits");
+        }
+    }
+    // 4. hashed N+(v) tables of the vertices with |N+(v)| >= nh_min (load-time derived data)
+    if (knobs().nhash_min > 0 && nnz > 0) {
+        DevBuf<int64_t> nb, excl;
+        nb.ensure(n, s);
+        excl.ensure(n + 1, s);
+        k_nh_sizes<<<grid_for(n), 256, 0, s>>>(g.off, g.up, n, knobs().nhash_min, nb.p);
+        GSM_LAUNCH("k_nh_sizes");
+        GSM_CUDA(cudaMemsetAsync(excl.p, 0, sizeof(int64_t), s));
+        size_t sb = 0;
+        GSM_CUDA(cub::DeviceScan::InclusiveSum(nullptr, sb, nb.p, excl.p + 1, n, s));
+        DevBuf<uint8_t> stmp;
+        stmp.ensure(sb, s);
+        GSM_CUDA(cub::DeviceScan::InclusiveSum(stmp.p, sb, nb.p, excl.p + 1, n, s));
+        int64_t total = 0;
+        GSM_CUDA(cudaMemcpyAsync(&total, excl.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        GSM_CUDA(cudaStreamSynchronize(s));
+        if (total > 0 && total < (int64_t)INT32_MAX) {
+            g.nh_min = knobs().nhash_min;
+            g.nh_buckets_total = total;
+            g.nh_off = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
+            g.nh_tab = static_cast<int32_t*>(dev_alloc(32 * (size_t)total, s));
+            GSM_CUDA(cudaMemsetAsync(g.nh_tab, 0xff, 32 * (size_t)total, s));
+            k_nh_offsets<<<grid_for(n), 256, 0, s>>>(nb.p, excl.p, n, g.nh_off);
+            GSM_LAUNCH("k_nh_offsets");
+            k_nh_insert<<<grid_for(n * 32), 256, 0, s>>>(g.off, g.cols, g.up, g.nh_off, n, g.nh_tab);
+            GSM_LAUNCH("k_nh_insert");
         }
     }
     if (labels) {

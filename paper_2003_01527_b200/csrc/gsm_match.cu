@@ -356,6 +356,8 @@ void Matcher::run() {
         cr.hub_bits = g_.hub_bits;
         cr.hub_base = g_.hub_base;
         cr.hub_words = g_.hub_words;
+        cr.nh_off = g_.nh_off;
+        cr.nh_tab = g_.nh_tab;
         int64_t launches = 0;
         rec_.run(GSM_K_CLIQUE, 1, [&] { launches = run_clique(cr, s_); });
         res_->kernel_launches += launches > 0 ? launches - 1 : 0;

@@ -152,7 +152,7 @@ def dense_gnp():
 
 
 @pytest.mark.parametrize("variant", ["default", "nohub", "hubmix", "hubmix_warp0", "warp0", "dsmem64", "search",
-                                     "stream", "nohash", "handback", "off"])
+                                     "stream", "nohash", "handback", "off", "nh_all", "nh_all_warp0", "nh_dsmem64"])
 def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
     """K3/K4 COUNT through the per-root local-bitmap kernels (gsm_clique.cu) in every
     bucket (warp per root; CTA with shared memory; CTA with a global slab via a tiny
@@ -163,15 +163,23 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
     "default" = every vertex of these small graphs is a hub, so every row is built by
     bitmap lookups; "hubmix" = only the top 256 ranks are hubs (lookup, stream and search
     rows mixed in one root); every other variant switches the bitmap off (GSM_HUB_BITS=0)
-    so its stream / search / bucket path is the one under test."""
+    so its stream / search / bucket path is the one under test.  Hashed N+(v) tables (read at
+    load time, GSM_NHASH_MIN): "nh_all*" give every non-empty list a table and force every row
+    onto table lookups (GSM_CLIQUE_NH_STREAM=0) in the warp, shared-memory and global-slab
+    kernels; the stream / search variants switch the tables off."""
     env = {"nohub": {}, "hubmix": {"GSM_HUB_BITS": "256"},
            "hubmix_warp0": {"GSM_HUB_BITS": "256", "GSM_CLIQUE_WARP": "0", "GSM_CLIQUE_DSMEM": "64"},
            "warp0": {"GSM_CLIQUE_WARP": "0"}, "dsmem64": {"GSM_CLIQUE_DSMEM": "64"},
            "search": {"GSM_CLIQUE_STREAM": "0"}, "stream": {"GSM_CLIQUE_STREAM": "1000000000"},
            "nohash": {"GSM_CLIQUE_HASH": "0"}, "handback": {"GSM_CLIQUE_DMAX": "64"},
-           "off": {"GSM_CLIQUE": "0"}}.get(variant, {})
+           "off": {"GSM_CLIQUE": "0"},
+           "nh_all": {"GSM_NHASH_MIN": "1", "GSM_CLIQUE_NH_STREAM": "0"},
+           "nh_all_warp0": {"GSM_NHASH_MIN": "1", "GSM_CLIQUE_NH_STREAM": "0", "GSM_CLIQUE_WARP": "0"},
+           "nh_dsmem64": {"GSM_NHASH_MIN": "1", "GSM_CLIQUE_NH_STREAM": "0", "GSM_CLIQUE_DSMEM": "64"}}.get(variant, {})
     if variant not in ("default", "hubmix", "hubmix_warp0"):
         env = {"GSM_HUB_BITS": "0", **env}
+    if variant not in ("default", "hubmix", "hubmix_warp0") and not variant.startswith("nh_"):
+        env = {"GSM_NHASH_MIN": "0", **env}
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = gi.rmat(10, 16, seed=12)
@@ -199,14 +207,14 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
         G.free()
 
 
-@pytest.mark.parametrize("pair", ["1", "warp", "0", "plan_thread", "nohub", "swap1", "swap1_warp"])
+@pytest.mark.parametrize("pair", ["1", "warp", "0", "plan_groups", "nohub", "swap1", "swap1_warp"])
 def test_pair_tail(pair, monkeypatch):
     """COUNT mode with the last two positions an independent pair (k_pair: |Cp||Cq| - |Cp∩Cq|)
     against the oracle's count, labeled and unlabeled, with and without symmetry; "0" =
     the pair ordering disabled (GSM_PAIR_TAIL=0) on the same inputs; "warp" = every row through
     the warp-per-row kernel (no thread-per-row pass)."""
-    if pair == "plan_thread":  # row plans by one thread per row instead of lane groups
-        monkeypatch.setenv("GSM_PLAN_GROUPS", "0")
+    if pair == "plan_groups":  # row plans by lane groups instead of one thread per row (the default)
+        monkeypatch.setenv("GSM_PLAN_GROUPS", "1")
     # membership tests: these small graphs are all hubs by default (bitmap tests); "nohub" = binary
     # searches only; "swap1" = search the image in N(v) whenever v's list is the shorter one
     if pair in ("nohub", "swap1", "swap1_warp"):

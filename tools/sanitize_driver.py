@@ -30,6 +30,12 @@ def main():
     print("K4 order1", m(G, gi.query("K4")))
     G.free()
     del os.environ["GSM_ORDER"]
+    os.environ["GSM_NHASH_MIN"] = "1"  # hashed N+(v) lookups in every clique row
+    os.environ["GSM_CLIQUE_NH_STREAM"] = "0"
+    G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, None)
+    print("K4 nh", m(G, gi.query("K4")), "K3 nh", m(G, gi.query("K3")))
+    G.free()
+    del os.environ["GSM_NHASH_MIN"], os.environ["GSM_CLIQUE_NH_STREAM"]
     os.environ["GSM_HUB_BITS"] = "0"
     os.environ["GSM_CLIQUE_DSMEM"] = "64"  # global-slab kernel
     G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, None)

@@ -49,6 +49,8 @@ def parse_args():
     p.add_argument("--clique", type=int, default=1, help="0: K3/K4 take the breadth-first path (GSM_CLIQUE=0)")
     p.add_argument("--lookahead", type=int, default=0, help="k-look-ahead depth (0/1/2)")
     p.add_argument("--compressed", action="store_true", help="compressed partial results")
+    p.add_argument("--shard-level", type=int, default=1, choices=[0, 1],
+                   help="N>1: shard by root (0) or by level-1 pair where level 1 is a breadth-first expand (1)")
     return p.parse_args()
 
 
@@ -300,7 +302,9 @@ def config_of(w, g, refine_rounds=0, args=None):
     extra = {}
     if args is not None:
         extra = {"match_mode": args.mode, "clique_path": bool(args.clique), "lookahead": args.lookahead,
-                 "compressed_partials": bool(args.compressed)}
+                 "compressed_partials": bool(args.compressed),
+                 "sharding": "level-1 pairs where level 1 is a breadth-first expand, else roots"
+                             if args.shard_level == 1 else "roots (rank % P)"}
     return {"workload": f"{w.name} (BASELINE configs[{w.config_index}]): {w.description}",
             "refine_rounds": refine_rounds, **extra,
             "graph": {"name": g.name, "num_nodes": g.num_nodes, "directed_edges": g.nnz,
@@ -346,6 +350,8 @@ def run_ours(args, world, rank, local, dist):
 
     enumerate_ = args.mode == "enumerate"
     extra_flags = gsm.GSM_FLAG_COMPRESSED_PARTIALS if args.compressed else 0
+    if world > 1 and args.shard_level == 1:
+        extra_flags |= gsm.GSM_FLAG_SHARD_LEVEL1
     host_rows = {}  # e2e (enumerate): pinned destination of each query's rows
 
     def step(flags, G_=None, d2h=False):

@@ -138,7 +138,14 @@ enum {
     /* store intermediate partial results as level-wise (parent row, vertex) pairs — 8 bytes per
        partial result at any width instead of 4 x width (PAPER P:136/"store the value
        to partial results ... to further save memory usage"; bijective, so listings are exact) */
-    GSM_FLAG_COMPRESSED_PARTIALS = 16u
+    GSM_FLAG_COMPRESSED_PARTIALS = 16u,
+    /* multi-GPU skew (SURVEY §8(e) mitigation): with num_shards = P > 1, shard by the LEVEL-1
+       partial result instead of the root: every rank expands all roots one level and keeps the
+       pairs (f(π[0]), f(π[1])) whose hash mod P == shard_index, so one hub root's subtree is
+       spread over all ranks.  Each embedding still belongs to exactly one shard.  Applies where
+       level 1 is a breadth-first expand (k >= 3, not the clique bitmap path, not a pair/fused
+       tail at level 1); elsewhere the call shards by root as without the flag. */
+    GSM_FLAG_SHARD_LEVEL1 = 32u
 };
 
 typedef struct {
@@ -218,6 +225,7 @@ typedef struct {
     uint64_t level_frontier_bytes[GSM_MAX_QUERY_NODES]; /* bytes of the stored partial results of each
                                 width w = i+1 (summed over chunks; plain 4w, compressed 8 per row) */
     int32_t compressed;      /* 1 if intermediate partial results used the compressed layout */
+    int32_t level1_sharded;  /* 1 if GSM_FLAG_SHARD_LEVEL1 sharded this call by level-1 pairs */
 } gsm_result;
 
 /*

@@ -82,7 +82,24 @@ struct LevelPlan {
     int32_t la_depth;    // 0 (off), 1 or 2
     int32_t nla;
     int32_t la_u[kMaxK];
+    // level-1 sharding (GSM_FLAG_SHARD_LEVEL1, position 1 only): keep the survivors v of row r
+    // with pair_shard(f_r(0), v, shard_p) == shard_s; shard_p <= 1 = off
+    int32_t shard_p;
+    int32_t shard_s;
 };
+
+#ifdef __CUDACC__
+#define GSM_HD __host__ __device__ __forceinline__
+#else
+#define GSM_HD inline
+#endif
+GSM_HD int32_t pair_shard(int32_t a, int32_t b, int32_t P) {
+    uint32_t h = (uint32_t)a * 0x9E3779B1u ^ ((uint32_t)b + 0x7F4A7C15u) * 0x85EBCA6Bu;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    return (int32_t)(h % (uint32_t)P);
+}
 
 LevelPlan make_level_plan(const QueryPlan& p, int i, bool count_only);
 

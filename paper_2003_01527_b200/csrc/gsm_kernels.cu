@@ -945,6 +945,11 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
                     }
                 }
             }
+            if (L.shard_p > 1) {  // level-1 sharding: this rank's (f(π[0]), f(π[1])) pairs only
+#pragma unroll
+                for (int j = 0; j < U; ++j)
+                    if (ok[j]) ok[j] = pair_shard(sRow[lr[j] * W] & L.idmask, v[j], L.shard_p) == L.shard_s;
+            }
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 if (kCountOnly) {

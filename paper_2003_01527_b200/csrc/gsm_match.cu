@@ -299,6 +299,16 @@ void Matcher::run() {
         lq_.ninj = n;
     }
 
+    // ---- level-1 sharding (GSM_FLAG_SHARD_LEVEL1): every rank takes all roots and keeps its
+    //      share of the (f(π[0]), f(π[1])) pairs, where level 1 is a breadth-first expand
+    const bool level1 = (opts_.flags & GSM_FLAG_SHARD_LEVEL1) && opts_.num_shards > 1 && !opts_.root_subset &&
+                        !clique_ && k_ >= 3 && !((pair_ || tail_) && k_ - 2 == 1);
+    if (level1) {
+        lplan_[1].shard_p = opts_.num_shards;
+        lplan_[1].shard_s = opts_.shard_index;
+    }
+    res_->level1_sharded = level1 ? 1 : 0;
+
     // ---- roots = C(π[0]) (level-0 frontier)
     int64_t R0 = 0;
     if (!empty && (int64_t)k_ <= g_.n) {
@@ -314,7 +324,7 @@ void Matcher::run() {
                                         lv_[1]->rows.p, s_);
             });
         } else {
-            const int nsh = opts_.num_shards > 1 ? opts_.num_shards : 1;
+            const int nsh = (opts_.num_shards > 1 && !level1) ? opts_.num_shards : 1;
             const int sh = nsh > 1 ? opts_.shard_index : 0;
             lv_[1]->rows.ensure(g_.n, s_);
             rec_.run(GSM_K_ROOTS, 3, [&] {

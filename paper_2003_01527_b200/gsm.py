@@ -29,6 +29,7 @@ GSM_FLAG_NO_SYMMETRY = 2
 GSM_FLAG_PROFILE = 4
 GSM_FLAG_PLAN_COUNT = 8
 GSM_FLAG_COMPRESSED_PARTIALS = 16
+GSM_FLAG_SHARD_LEVEL1 = 32
 KERNEL_NAMES = ["filter", "roots", "plan", "scan", "expand", "finalize", "tail", "clique"]
 
 
@@ -69,7 +70,8 @@ class gsm_result(ctypes.Structure):
                 ("level_rows", ctypes.c_uint64 * MAX_K), ("level_work", ctypes.c_uint64 * MAX_K),
                 ("num_chunks", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("prof", gsm_kernel_prof * 8), ("device", ctypes.c_int32), ("symmetric", ctypes.c_int32),
-                ("level_frontier_bytes", ctypes.c_uint64 * MAX_K), ("compressed", ctypes.c_int32)]
+                ("level_frontier_bytes", ctypes.c_uint64 * MAX_K), ("compressed", ctypes.c_int32),
+                ("level1_sharded", ctypes.c_int32)]
 
 
 class gsm_plan_info(ctypes.Structure):
@@ -223,6 +225,7 @@ class Result:
         self.level_rows = [int(x) for x in r.level_rows[:k]]
         self.level_frontier_bytes = [int(x) for x in r.level_frontier_bytes[:k]]
         self.compressed = bool(r.compressed)
+        self.level1_sharded = bool(r.level1_sharded)
         self.level_work = [int(x) for x in r.level_work[:k]]
         self.num_chunks = int(r.num_chunks)
         self.kernel_launches = int(r.kernel_launches)

@@ -515,6 +515,42 @@ def test_shard_invariance():
         G.free()
 
 
+def test_level1_shard_invariance(monkeypatch):
+    """GSM_FLAG_SHARD_LEVEL1 (SURVEY §8(e) skew mitigation): P shards of the level-1 pairs run
+    sequentially on one GPU — counts add up to the oracle's, the rows' union is the oracle's
+    list, each shard really was pair-sharded (where level 1 is a breadth-first expand) and a
+    single hub root's embeddings are split over several shards."""
+    g = gi.rmat(10, 8, seed=3).with_labels(gi.uniform_labels(1024, 2, 3))
+    G = load(g)
+    F = gsm.GSM_FLAG_SHARD_LEVEL1
+    try:
+        for q in [gi.query("P4", [0, 1, 1, 0]), gi.query("house", [0, 1, 0, 1, 0]), gi.query("C4"), gi.query("K4")]:
+            cnt, ref = oracle.match(g, q)
+            for P in (2, 3, 8):
+                tot = 0
+                parts = []
+                for s in range(P):
+                    c, rows, r = run(G, q, "enumerate", flags=F, shard_index=s, num_shards=P)
+                    assert r.level1_sharded
+                    cc, _, rc = run(G, q, "count", flags=F, shard_index=s, num_shards=P)
+                    assert cc == c, (q.name, P, s)
+                    tot += c
+                    parts.append(rows)
+                assert tot == cnt
+                assert_rows_equal(oracle.sort_rows(np.concatenate(parts)), ref, f"{q.name} P={P} level1")
+        # the COUNT-mode clique path stays root-sharded (flag ignored), still exact
+        q = gi.query("K4")
+        cnt, _ = oracle.match(g, q, count_only=True)
+        tot = 0
+        for s in range(4):
+            c, _, r = run(G, q, "count", flags=F, shard_index=s, num_shards=4)
+            assert not r.level1_sharded and r.prof["clique"]["launches"] > 0
+            tot += c
+        assert tot == cnt
+    finally:
+        G.free()
+
+
 def test_root_subset_sampling():
     g = gi.rmat(12, 16, seed=6).with_labels(gi.uniform_labels(4096, 3, 6))
     G = load(g)

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--workload", default="rmat24")
     ap.add_argument("--shards", type=int, default=8)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--level1", action="store_true", help="GSM_FLAG_SHARD_LEVEL1: shard by level-1 pairs")
     args = ap.parse_args()
     import torch
 
@@ -34,7 +35,8 @@ def main():
     g = w.graph()
     G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=0)
     stream = torch.cuda.current_stream()
-    out = {"workload": args.workload, "shards": args.shards, "queries": {}}
+    out = {"workload": args.workload, "shards": args.shards, "level1": bool(args.level1), "queries": {}}
+    sflags = gsm.GSM_FLAG_SHARD_LEVEL1 if args.level1 else 0
 
     def timed(q, **kw):
         ms = []
@@ -56,9 +58,11 @@ def main():
         rows = []
         tot = 0
         for s in range(args.shards):
-            r, ms = timed(q, shard_index=s, num_shards=args.shards)
+            r, ms = timed(q, shard_index=s, num_shards=args.shards, flags=sflags)
             tot += r.count
-            rows.append({"shard": s, "ms": round(ms, 3), "count": r.count, "roots": r.level_rows[0]})
+            rows.append({"shard": s, "ms": round(ms, 3), "count": r.count, "roots": r.level_rows[0],
+                         "level1_rows": r.level_rows[1] if len(r.level_rows) > 1 else None,
+                         "level1_sharded": r.level1_sharded})
             per_shard_step[s] += ms
         assert tot == r_all.count, (q.name, tot, r_all.count)
         mss = [x["ms"] for x in rows]

@@ -145,7 +145,7 @@ struct Knobs {
     int plan_groups = 0;      // GSM_PLAN_GROUPS: row plans by lane groups (R-MAT-22 plan 19.6 vs 15.5 ms: off)
     int compress = -1;        // GSM_COMPRESS: 1/0 force the compressed partial layout on/off (-1 = flag)
     int lookahead = -1;       // GSM_LOOKAHEAD: overrides gsm_match_opts.lookahead when >= 0
-    int hub_bits = 32768;     // GSM_HUB_BITS: H of the hub adjacency bitmap built at load (0 = none)
+    int hub_bits = 65536;     // GSM_HUB_BITS: H of the hub adjacency bitmap built at load (0 = none; R-MAT-24: 32k 378, 64k 364 ms)
     int clique_hub = 1;       // GSM_CLIQUE_HUB: clique rows of a hub pivot by bitmap lookups
     int clique_hub_ratio = 64;  // GSM_CLIQUE_HUB_RATIO: lookups when 32 nj <= ratio |N+(S[i])|
     int nhash_min = 16;       // GSM_NHASH_MIN (read at gsm_load_graph): hashed N+(v) for |N+(v)| >= this (0 = none)

@@ -9,6 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libgsm.so")
+SO_CHECKED = os.path.join(HERE, "libgsm_checked.so")  # -DGSM_DEVICE_CHECKS (tests only)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -23,21 +24,26 @@ def deps():
     return sources() + glob.glob(os.path.join(c, "*.h")) + [os.path.join(ROOT, "include", "gsm.h")]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(SO):
+def up_to_date(so: str = SO) -> bool:
+    if not os.path.exists(so):
         return False
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return SO
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """libgsm.so; checked=True: libgsm_checked.so with the device index checks compiled in
+    (GSM_DEVICE_CHECKS, gsm_common.h) — a test build, selected by GSM_LIB=checked."""
+    so = SO_CHECKED if checked else SO
+    if not force and up_to_date(so):
+        return so
+    objdir = os.path.join(HERE, "build_checked" if checked else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
               "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc")]
+    if checked:
+        common.append("-DGSM_DEVICE_CHECKS")
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
@@ -54,10 +60,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(out)
     if failed:
         raise RuntimeError("libgsm build failed")
-    tmp = SO + f".tmp{os.getpid()}"
+    tmp = so + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC"])
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    return so
 
 
 if __name__ == "__main__":

@@ -100,8 +100,8 @@ struct BucketEdges {
 
 // keys[r] = |N+(roots[r])| (0 if below k-1: no clique through it), vals[r] = r; bucket
 // counts and the max.  Descending keys keep every bucket contiguous in the sorted order.
-__global__ void k_clique_keys(const int32_t* __restrict__ roots, int64_t R, const int64_t* __restrict__ off,
-                              const int32_t* __restrict__ up, int kmin, BucketEdges E, int32_t* __restrict__ keys,
+__global__ void k_clique_keys(const int32_t* __restrict__ roots, int64_t R, const int4* __restrict__ np,
+                              int kmin, BucketEdges E, int32_t* __restrict__ keys,
                               int32_t* __restrict__ vals, unsigned long long* __restrict__ bucket, int* dmax) {
     __shared__ unsigned long long sb[8];
     __shared__ int sm, small;
@@ -111,7 +111,7 @@ __global__ void k_clique_keys(const int32_t* __restrict__ roots, int64_t R, cons
     int lm = 0, lall = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
         const int32_t u = roots[r];
-        int d = (int)(off[u + 1] - off[u] - up[u]);
+        int d = __ldg(np + u).z;
         if (d < kmin) d = 0;
         keys[r] = d;
         vals[r] = (int32_t)r;
@@ -138,6 +138,7 @@ struct CliqueArgs {
     const int64_t* off;
     const int32_t* cols;
     const int32_t* up;
+    const int4* np;         // DevGraph::nplus: packed {begin, |N+(v)|, nh_off} per vertex
     int32_t dmax;           // max |N+(u)| of this launch (sizes shared memory / the slab)
     int32_t stream_max;     // row construction streams N+(S[i]) when its length <= stream_max * (#j)/32
     int32_t use_hash;       // k_clique_cta: cuckoo table of S(u) (0: rows by binary search only)
@@ -149,6 +150,7 @@ struct CliqueArgs {
     const int32_t* nh_tab;
     int32_t nh_stream;      // with a table, a row streams N+(S[i]) only when 32 |N+(S[i])| <= nh_stream x nj
     int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
+    int32_t slab_blocks;    // kGlobal: slabs allocated (the grid must not exceed it)
     unsigned long long* next;   // dynamic root scheduler
     unsigned long long* count;  // unique cliques (atomic)
     unsigned long long* stats;  // [list entries read, global probes, bitmap words, cliques, sum |S(u)|]
@@ -167,9 +169,18 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
     const int64_t nw = (int64_t)gridDim.x * 8;
     for (int64_t t = (int64_t)blockIdx.x * 8 + wib; t < a.n; t += nw) {
         const int32_t u = a.roots[a.idx[t]];
-        const int64_t s0 = a.off[u] + a.up[u];
-        const int d = (int)(a.off[u + 1] - s0);
+        int64_t s0;
+        int d;
+        int32_t unh;
+        nplus_load(a.np, u, s0, d, unh);
+        (void)unh;
+        GSM_DCHECK(d <= 32, DCHK_WARP_D);
         const int32_t sv = lane < d ? cols[s0 + lane] : INT32_MAX;
+        // each lane's own S entry's N+ descriptor (rows broadcast it by shuffle)
+        int64_t my_b = 0;
+        int my_len = 0;
+        int32_t my_nh = -1;
+        if (lane < d) nplus_load(a.np, sv, my_b, my_len, my_nh);
         sS[wib][lane] = sv;
         if (lane == 0) sent += d;
         __syncwarp();
@@ -177,7 +188,9 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
         unsigned myrow = 0;
         for (int i = 0; i < d - 1; ++i) {
             const int32_t ai = sS[wib][i];
-            const int64_t ls = a.off[ai] + a.up[ai], le = a.off[ai + 1];
+            const int64_t ls = __shfl_sync(kFull, my_b, i);
+            const int64_t le = ls + __shfl_sync(kFull, my_len, i);
+            const int32_t ai_nh = __shfl_sync(kFull, my_nh, i);
             const int nj = d - 1 - i;
             unsigned bits = 0;
             if (a.hub_bits && ai >= a.hub_base) {
@@ -191,9 +204,9 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
                 }
                 bits = __ballot_sync(kFull, f);
                 items += live;
-            } else if (a.nh_off && 32 * (le - ls) > (int64_t)a.nh_stream * nj && __ldg(a.nh_off + ai) >= 0) {
+            } else if (ai_nh >= 0 && 32 * (le - ls) > (int64_t)a.nh_stream * nj) {
                 // hashed N+(S[i]): one bucket (32-byte sector) per remaining S[j]
-                const int32_t tb = __ldg(a.nh_off + ai);
+                const int32_t tb = ai_nh;
                 const bool live = lane > i && lane < d;
                 const bool f = live && nh_find(a.nh_tab, tb, nh_buckets(le - ls), sv, probes);
                 bits = __ballot_sync(kFull, f);
@@ -274,7 +287,7 @@ __host__ __device__ inline int64_t tri_words(int d) {
 }
 
 struct CtaLay {
-    int64_t h, tb, s, rl, rb, A;  // offsets (int32 units) in shared memory or the slab
+    int64_t h, tb, s, rl, rh, rb, A;  // offsets (int32 units) in shared memory or the slab
     int64_t smem_ints, slab_ints;
 };
 
@@ -291,6 +304,8 @@ __host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool has
     L.s = q;
     q += dmax;
     L.rl = q;
+    q += dmax;
+    L.rh = q;
     q += dmax;
     q = (q + 1) & ~1LL;  // int64 alignment
     L.rb = q;
@@ -319,6 +334,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     int32_t* TB = csm + L.tb;  // TB[b] = first word of row block b, TB[W + 1 + b] = its row length
     int32_t* S = ws + L.s;
     int32_t* RL = ws + L.rl;
+    int32_t* RH = ws + L.rh;  // nh_off of each S entry (-1: no hashed N+)
     int64_t* RB = reinterpret_cast<int64_t*>(ws + L.rb);
     unsigned* A = reinterpret_cast<unsigned*>(ws + L.A);
     unsigned long long cnt = 0, items = 0, words = 0, sent = 0;
@@ -337,8 +353,19 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         const int64_t t = (int64_t)sRoot;
         if (t >= a.n) break;
         const int32_t u = a.roots[a.idx[t]];
-        const int64_t s0 = a.off[u] + a.up[u];
-        const int d = (int)(a.off[u + 1] - s0);
+        int64_t s0;
+        int d;
+        int32_t unh;
+        nplus_load(a.np, u, s0, d, unh);
+        (void)unh;
+#ifdef GSM_DEVICE_CHECKS
+        if (d > a.dmax) {  // the launch's shared memory / slab is sized for dmax
+            GSM_DCHECK(false, DCHK_CTA_D);
+            continue;
+        }
+        GSM_DCHECK(!kGlobal || blockIdx.x < (unsigned)a.slab_blocks, DCHK_SLAB);
+        const int64_t tri_lim = K == 4 ? tri_words(d) : 0;
+#endif
         const int W = (d + 31) >> 5;
         const unsigned P = cuckoo_slots(d);
         if (K == 4 && threadIdx.x < W) {
@@ -352,9 +379,13 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         for (int j = threadIdx.x; j < d; j += NT) {
             const int32_t v = cols[s0 + j];
             S[j] = v;
-            const int64_t b = a.off[v] + a.up[v];
+            int64_t b;
+            int len;
+            int32_t nh;
+            nplus_load(a.np, v, b, len, nh);
             RB[j] = b;
-            RL[j] = (int)(a.off[v + 1] - b);
+            RL[j] = len;
+            RH[j] = nh;
         }
         if (threadIdx.x == 0) sent += d;
         // cuckoo build (a failed build — an eviction cycle — retries with a new seed; after
@@ -375,6 +406,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 int it = 0;
                 for (; it < 64; ++it) {
                     const unsigned slot = tbl ? P + ck_h1(e, P, seed) : ck_h0(e, P, seed);
+                    GSM_DCHECK(slot < 2 * P, DCHK_CUCKOO);
                     e = atomicExch(&Tk[slot], e);
                     if (e == -1) break;
                     tbl ^= 1;
@@ -410,6 +442,9 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             if (i >= d) break;
             const int w0 = i >> 5;
             unsigned* Ai = A + TB[w0] + (i & 31) * TB[W + 1 + w0] - w0;  // Ai[w], w >= w0
+#ifdef GSM_DEVICE_CHECKS
+            GSM_DCHECK(K != 4 || (Ai + w0 >= A && Ai + W <= A + tri_lim), DCHK_AROW);
+#endif
             if (i == d - 1) {  // no j > i: an all-zero row (read by level 3)
                 if (K == 4 && lane == 0) Ai[w0] = 0;
                 continue;
@@ -448,7 +483,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             }
             // hashed N+(S[i]) (load-time table): one 32-byte bucket per remaining S[j], unless
             // streaming the list is cheaper (32 len <= nh_stream x nj)
-            const int32_t tb = a.nh_off ? __ldg(a.nh_off + ai) : -1;
+            const int32_t tb = RH[i];
             if (tb >= 0 && !(use_ck && (int64_t)len * 32 <= (int64_t)a.nh_stream * nj)) {
                 const unsigned B = nh_buckets(len);
                 for (int w = w0; w < W; ++w) {
@@ -569,6 +604,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                         const int rank = __popc(bits & ((1u << lane) - 1u));
                         const bool tk = has && rank < take;
                         if (tk) {
+                            GSM_DCHECK(nJ + rank < 32, DCHK_PAIRQ);
                             sJ[wib][nJ + rank] = (w << 5) + lane;
                             sJ[wib][32 + nJ + rank] = i;
                         }
@@ -703,7 +739,7 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     GSM_CUDA(cudaMemsetAsync(sched.p, 0, sizeof(unsigned long long) * kNB, s));
     const int sms = sm_count();
     k_clique_keys<<<(unsigned)std::min<int64_t>((R + 255) / 256, (int64_t)sms * 8), 256, 0, s>>>(
-        r.roots, R, r.off, r.up, K - 1, E, keys.p, vals.p, bucket.p, dmax.p);
+        r.roots, R, r.nplus, K - 1, E, keys.p, vals.p, bucket.p, dmax.p);
     GSM_LAUNCH("k_clique_keys");
     unsigned long long hb[kNB];
     int hm[2] = {0, 0};
@@ -728,6 +764,7 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     a.off = r.off;
     a.cols = r.cols;
     a.up = r.up;
+    a.np = r.nplus;
     a.stream_max = stream_max();
     a.use_hash = use_hash();
     a.hub_bits = knobs().clique_hub ? r.hub_bits : nullptr;
@@ -745,6 +782,7 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
         a.cyc = cyc.p;
     }
     a.slab = nullptr;
+    a.slab_blocks = 0;
     a.count = r.count;
     a.stats = r.stats;
     // sorted descending: [bucket kNB-1 (handed back) | kNB-2 | ... | 0]
@@ -775,6 +813,7 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
             const CtaLay L = cta_lay(K, a.dmax, true, a.use_hash != 0);
             slab.ensure((size_t)blocks * L.slab_ints, s);
             a.slab = slab.p;
+            a.slab_blocks = (int32_t)blocks;
             launch_cta<K, true, 1024>(a, blocks, s);
         } else {
             // CTA size with the most resident warps per SM for this bucket's shared memory

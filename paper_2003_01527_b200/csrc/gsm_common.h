@@ -13,6 +13,48 @@
 
 namespace gsm {
 
+// ---------------------------------------------------------------- device checks
+// Build with -DGSM_DEVICE_CHECKS (libgsm_checked.so, _build.build(checked=True)): kernels test
+// their shared-memory / staging / table indices against the sizes they were launched with and
+// OR a bit into a per-translation-unit device flag instead of touching memory out of bounds
+// unchecked; gsm_match collects the flags after every call and fails with GSM_ERR_CUDA
+// ("device check failed") if any is set.  The stand-in for compute-sanitizer, which this
+// GPU pool does not allow.  Release builds compile the checks away.
+#ifdef GSM_DEVICE_CHECKS
+void dcheck_register(unsigned (*read_and_clear)());
+unsigned dcheck_collect();
+#ifdef __CUDACC__
+static __device__ unsigned int g_dcheck_tu;
+static unsigned dcheck_read_tu() {
+    unsigned h = 0, z = 0;
+    cudaMemcpyFromSymbol(&h, g_dcheck_tu, sizeof(h));
+    cudaMemcpyToSymbol(g_dcheck_tu, &z, sizeof(z));
+    return h;
+}
+static const bool g_dcheck_registered = (dcheck_register(&dcheck_read_tu), true);
+#define GSM_DCHECK(cond, bit)                                            \
+    do {                                                                 \
+        if (!(cond)) atomicOr(&::gsm::g_dcheck_tu, (unsigned)(bit));     \
+    } while (0)
+#endif
+#else
+#define GSM_DCHECK(cond, bit) \
+    do {                      \
+    } while (0)
+#endif
+enum : unsigned {
+    DCHK_WARP_D = 1u,        // k_clique_warp root with |N+(u)| > 32
+    DCHK_CTA_D = 2u,         // k_clique_cta root beyond the launch's dmax
+    DCHK_CUCKOO = 4u,        // cuckoo slot outside the 2P table
+    DCHK_PAIRQ = 8u,         // level-3 pair queue index >= 32
+    DCHK_AROW = 16u,         // bit-row word outside the triangular row block
+    DCHK_SLAB = 32u,         // global-slab CTA beyond the slabs allocated
+    DCHK_STAGE = 64u,        // k_expand staging slot / row index beyond the tile capacity
+    DCHK_NH = 128u,          // hashed N+(v) probe walked more buckets than the table has
+    DCHK_MERGE = 256u,       // merge-path output index beyond na + nb
+};
+
+
 // Relabelled device CSR (new ids = rank by ascending (degree, original id)).
 struct DevGraph {
     int64_t n = 0;
@@ -47,6 +89,10 @@ struct DevGraph {
     // log2 |N+(v)| dependent probes.  nullptr = disabled (GSM_NHASH_MIN=0).
     int32_t* nh_off = nullptr;
     int32_t* nh_tab = nullptr;
+    // packed N+(v) descriptor per vertex, one 16-byte load: {begin lo, begin hi, |N+(v)|, nh_off}
+    // (begin = off[v] + up[v]); read by the clique kernels instead of off[v], off[v+1], up[v]
+    // and nh_off[v] (three to four random sectors -> one)
+    int4* nplus = nullptr;
     int64_t nh_buckets_total = 0;
     int32_t nh_min = 0;
 };
@@ -61,11 +107,24 @@ __host__ __device__ __forceinline__ unsigned nh_hash(int32_t x, unsigned B) {
     return ((unsigned)x * 0x9E3779B1u) & (B - 1);  // B is a power of two
 }
 #ifdef __CUDACC__
+__device__ __forceinline__ void nplus_load(const int4* __restrict__ np, int32_t v, int64_t& begin, int& len,
+                                           int32_t& nh) {
+    const int4 x = __ldg(np + v);
+    begin = (int64_t)(uint32_t)x.x | ((int64_t)x.y << 32);
+    len = x.z;
+    nh = x.w;
+}
 // x ∈ N+(v), given v's table (first bucket tb) of B buckets: one 32-byte bucket per probe
 __device__ __forceinline__ bool nh_find(const int32_t* __restrict__ tab, int32_t tb, unsigned B, int32_t x,
                                         unsigned& probes) {
     unsigned b = nh_hash(x, B);
-    for (;;) {
+    for (unsigned it = 0;; ++it) {
+#ifdef GSM_DEVICE_CHECKS
+        if (it >= B) {  // a table always keeps an empty slot (load <= 1/2)
+            GSM_DCHECK(false, DCHK_NH);
+            return false;
+        }
+#endif
         const int4* p = reinterpret_cast<const int4*>(tab + 8 * ((int64_t)tb + b));
         const int4 u = __ldg(p), w = __ldg(p + 1);
         ++probes;

@@ -9,6 +9,7 @@
 // constraints) is plain integer '<' on new ids, and
 // N+(v) = {w in N(v) : v ≺ w} is the contiguous suffix of v's sorted list
 // starting at up[v].  Every id crossing the ABI is an original id.
+#include <vector>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -81,6 +82,19 @@ void load_knobs() {
     k.clique_nh_stream = env_or("GSM_CLIQUE_NH_STREAM", k.clique_nh_stream);
     g_knobs = k;
 }
+
+#ifdef GSM_DEVICE_CHECKS
+static std::vector<unsigned (*)()>& dcheck_readers() {
+    static std::vector<unsigned (*)()> v;
+    return v;
+}
+void dcheck_register(unsigned (*fn)()) { dcheck_readers().push_back(fn); }
+unsigned dcheck_collect() {
+    unsigned f = 0;
+    for (auto fn : dcheck_readers()) f |= fn();
+    return f;
+}
+#endif
 
 void* dev_alloc(size_t bytes, cudaStream_t s) {
     void* p = nullptr;
@@ -365,6 +379,15 @@ __global__ void k_nh_insert(const int64_t* __restrict__ off, const int32_t* __re
     }
 }
 
+__global__ void k_nplus(const int64_t* __restrict__ off, const int32_t* __restrict__ up,
+                        const int32_t* __restrict__ nh_off, int64_t n, int4* __restrict__ np) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = off[v] + up[v];
+        np[v] = make_int4((int32_t)(uint32_t)(b & 0xffffffffLL), (int32_t)(b >> 32), (int32_t)(off[v + 1] - b),
+                          nh_off ? nh_off[v] : -1);
+    }
+}
+
 // keys = (peeling round, degree, id) of the approximate degeneracy order (k_adg_*)
 static void adg_keys(const int64_t* off, const int32_t* cols, int64_t n, int64_t nnz, uint64_t* keys, cudaStream_t s) {
     (void)nnz;
@@ -420,7 +443,7 @@ static void free_graph(gsm_graph* h) {
     // graph arrays come from the device's stream-ordered pool (kept cached by its release
     // threshold, so a load/free/load cycle does not re-map memory)
     for (void* p : {(void*)g.off, (void*)g.cols, (void*)g.up, (void*)g.labels, (void*)g.lkeys, (void*)g.new2old,
-                    (void*)g.old2new, (void*)g.hub_bits, (void*)g.nh_off, (void*)g.nh_tab})
+                    (void*)g.old2new, (void*)g.hub_bits, (void*)g.nh_off, (void*)g.nh_tab, (void*)g.nplus})
         if (p) cudaFreeAsync(p, h->stream);
     cudaStreamSynchronize(h->stream);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -623,6 +646,9 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
             GSM_LAUNCH("k_nh_insert");
         }
     }
+    g.nplus = static_cast<int4*>(dev_alloc(sizeof(int4) * n, s));
+    k_nplus<<<grid_for(n), 256, 0, s>>>(g.off, g.up, g.nh_off, n, g.nplus);
+    GSM_LAUNCH("k_nplus");
     if (labels) {
         g.labels = static_cast<uint32_t*>(dev_alloc(sizeof(uint32_t) * n, s));
         k_permute_labels<<<grid_for(n), 256, 0, s>>>(d_lab, g.new2old, n, g.labels);

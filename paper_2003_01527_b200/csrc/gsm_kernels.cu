@@ -961,6 +961,7 @@ __global__ void __launch_bounds__(kThreads) k_expand(ExpandArgs a, LevelPlan L) 
                     wbase = __shfl_sync(0xffffffffu, wbase, 0);
                     if (ok[j]) {
                         const int pos = wbase + __popc(ball & ((1u << lane) - 1u));
+                        GSM_DCHECK(pos < TD && lr[j] <= (int)TD, DCHK_STAGE);
                         if (a.out_pv) {  // compressed: (input row index, vertex)
                             int32_t* o = sOut + (int64_t)pos * 2;
                             o[0] = (int32_t)(ra0 + lr[j]);

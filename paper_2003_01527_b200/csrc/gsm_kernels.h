@@ -217,6 +217,7 @@ struct CliqueRun {
     struct Workspace* ws;   // per-graph grow-only buffers (gsm_workspace.h)
     const uint32_t* hub_bits = nullptr;  // DevGraph hub bitmap (nullptr = none)
     int32_t hub_base = 0, hub_words = 0;
+    const int4* nplus = nullptr;      // DevGraph packed N+(v) descriptors
     const int32_t* nh_off = nullptr;  // DevGraph hashed N+(v) tables (nullptr = none)
     const int32_t* nh_tab = nullptr;
 };

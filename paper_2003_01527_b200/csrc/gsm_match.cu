@@ -367,6 +367,7 @@ void Matcher::run() {
         cr.hub_base = g_.hub_base;
         cr.hub_words = g_.hub_words;
         cr.nh_off = g_.nh_off;
+        cr.nplus = g_.nplus;
         cr.nh_tab = g_.nh_tab;
         int64_t launches = 0;
         rec_.run(GSM_K_CLIQUE, 1, [&] { launches = run_clique(cr, s_); });
@@ -909,6 +910,14 @@ void match_impl(const gsm_graph* gh, const gsm_query* q, const gsm_match_opts* u
     try {
         Matcher m(gh, plan, opts, out, s);
         m.run();
+#ifdef GSM_DEVICE_CHECKS
+        GSM_CUDA(cudaStreamSynchronize(s));
+        if (const unsigned f = dcheck_collect()) {
+            char buf[96];
+            std::snprintf(buf, sizeof(buf), "device check failed: flags 0x%x (gsm_common.h DCHK_*)", f);
+            fail(GSM_ERR_CUDA, buf);
+        }
+#endif
     } catch (...) {
         cudaStreamSynchronize(s);
         cudaSetDevice(prev);

@@ -41,6 +41,7 @@ __global__ void k_merge_rows(const int32_t* __restrict__ a, int64_t na, const in
         }
         int64_t i = lo, j = diag - lo;
         const int64_t end = diag + kPer < n ? diag + kPer : n;
+        GSM_DCHECK(i >= 0 && i <= na && j >= 0 && j <= nb, DCHK_MERGE);
         for (int64_t p = diag; p < end; ++p) {
             const bool take_a = j >= nb || (i < na && !row_less(b + j * w, a + i * w, w));
             const int32_t* src = take_a ? a + i * w : b + j * w;
@@ -81,6 +82,9 @@ gsm_status gsm_merge_rows(const int32_t* a, uint64_t na, const int32_t* b, uint6
         cudaStream_t s = (cudaStream_t)stream;
         gsm::merge_rows(a, (int64_t)na, b, (int64_t)nb, width, out, s);
         GSM_CUDA(cudaStreamSynchronize(s));
+#ifdef GSM_DEVICE_CHECKS
+        if (gsm::dcheck_collect()) gsm::fail(GSM_ERR_CUDA, "device check failed in gsm_merge_rows");
+#endif
         cudaSetDevice(prev);
         return GSM_OK;
     } catch (const gsm::Failure& f) {

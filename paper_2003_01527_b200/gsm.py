@@ -15,7 +15,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libgsm.so")
+# GSM_LIB=checked selects the device-index-checked test build (libgsm_checked.so)
+SO_PATH = os.path.join(HERE, "libgsm_checked.so" if os.environ.get("GSM_LIB") == "checked" else "libgsm.so")
 
 MAX_K = 32
 

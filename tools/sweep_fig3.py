@@ -75,15 +75,20 @@ def point(out, g, G, q, sweep, x, args):
     c, ms_mean, ms_med = time_match(G, q, args.reps)
     rec = {"sweep": sweep, "x": x, "graph": g.name, "query": q.name, "k": q.num_nodes, "edges": len(q.edges),
            "count": c, "gpu_ms_mean": ms_mean, "gpu_ms_median": ms_med, "oracle_threads": oracle.num_threads()}
+    if ms_med < 5000:  # second GPU search path: the direct search without ID constraints (all embeddings)
+        r = gsm.gsm_match(G, q.num_nodes, q.edges, q.labels, mode=gsm.GSM_MODE_COUNT, flags=gsm.GSM_FLAG_NO_SYMMETRY)
+        rec["nosym_count_equal"] = r.count == c
     res = oracle_bounded(g, q, None, args.oracle_s)
     if res is not None:
         rec.update(parity="full", oracle_count=res[0], oracle_s=res[1], match=c == res[0])
+    elif args.sample_roots <= 0:
+        rec.update(parity="none (full oracle over time limit)", match=None)
     else:
         n = g.num_nodes
         cnt = min(n, args.sample_roots)
         roots = np.unique((np.arange(cnt) * (n / cnt)).astype(np.int64)).astype(np.int32)
         cs, _, _ = time_match(G, q, 0, root_subset=roots)
-        res = oracle_bounded(g, q, roots, 4 * args.oracle_s)
+        res = oracle_bounded(g, q, roots, 3 * args.oracle_s)
         if res is None:
             rec.update(parity="none (oracle sample over time limit)", match=None)
         else:
@@ -99,7 +104,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--reps", type=int, default=10)
     p.add_argument("--oracle-s", type=float, default=20.0)
-    p.add_argument("--sample-roots", type=int, default=512)
+    p.add_argument("--sample-roots", type=int, default=32)
     p.add_argument("--queries", type=int, default=10, help="random-walk queries per label count (P:220)")
     p.add_argument("--out", default="gpurun_out/fig3_sweep.jsonl")
     a = p.parse_args()

@@ -494,6 +494,10 @@ def run_ours(args, world, rank, local, dist):
             "traffic_source": "profiles/ncu_summary.json: ncu dram__bytes_read.sum+dram__bytes_write.sum of all "
                               "kernels of this kind in a one-step capture / recorder launches per step",
             "peak_source": peaks.get("_source", "absent"),
+            "dram_gbs": (traffic / (kp["ms"] / max(1, kp["launches"]) / 1e3)) / 1e9
+                        if (traffic and kp["ms"] > 0) else None,
+            "dram_frac": (traffic / (kp["ms"] / max(1, kp["launches"]) / 1e3)) / 1e9 / peak
+                         if (traffic and kp["ms"] > 0 and peak) else None,
             "launches_per_step": kp["launches"] / args.steps,
             "kernel_ms_per_step": kp["ms"] / args.steps,
             "alg_bytes_per_launch": kp["alg_bytes"] / max(1, kp["launches"]),

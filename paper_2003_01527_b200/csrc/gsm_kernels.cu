@@ -71,32 +71,48 @@ __global__ void __launch_bounds__(kThreads) k_filter(const int64_t* __restrict__
         for (int u = 0; u < q.k; ++u) m |= (uint32_t)((!q.use_labels || lab == q.qlabel[u]) && d >= q.qdeg[u]) << u;
         return m;
     };
-    // grid-stride over groups; the loop bound is warp-uniform so the shuffles stay converged
-    for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x; g0 < nvec; g0 += stride) {
-        const int64_t gi = g0 + threadIdx.x;
-        const bool live = gi < nvec;
-        int64_t o[5] = {0, 0, 0, 0, 0};
-        uint4 lab = make_uint4(0, 0, 0, 0);
-        if (live) {
-            const longlong2 a = reinterpret_cast<const longlong2*>(off)[2 * gi];
-            const longlong2 b = reinterpret_cast<const longlong2*>(off)[2 * gi + 1];
-            o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
-            if (labels && q.use_labels) lab = reinterpret_cast<const uint4*>(labels)[gi];
+    // grid-stride over groups, kU groups per thread per pass with every load issued before any
+    // use (more bytes in flight per thread: ncu showed the one-group loop at 31 % of DRAM
+    // bandwidth, stalled on the shuffle that waits for the offsets); the loop bound is
+    // block-uniform so the shuffles stay converged
+    constexpr int kU = 4;
+    for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x; g0 < nvec; g0 += stride * kU) {
+        longlong2 A[kU], Bq[kU];
+        uint4 lab[kU];
+        int64_t last[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int64_t gi = g0 + j * stride + threadIdx.x;
+            A[j] = make_longlong2(0, 0);
+            Bq[j] = make_longlong2(0, 0);
+            lab[j] = make_uint4(0, 0, 0, 0);
+            last[j] = 0;
+            if (gi < nvec) {
+                A[j] = __ldcs(reinterpret_cast<const longlong2*>(off) + 2 * gi);
+                Bq[j] = __ldcs(reinterpret_cast<const longlong2*>(off) + 2 * gi + 1);
+                if (labels && q.use_labels) lab[j] = __ldcs(reinterpret_cast<const uint4*>(labels) + gi);
+                if (lane == 31 || gi + 1 >= nvec) last[j] = __ldg(off + 4 * gi + 4);
+            }
         }
-        const int64_t nxt = __shfl_down_sync(0xffffffffu, o[0], 1);
-        o[4] = (lane == 31 || gi + 1 >= nvec) ? (live ? off[4 * gi + 4] : 0) : nxt;
-        uint32_t m[4] = {0, 0, 0, 0};
-        if (live) {
-            m[0] = mask_of(o[1] - o[0], lab.x);
-            m[1] = mask_of(o[2] - o[1], lab.y);
-            m[2] = mask_of(o[3] - o[2], lab.z);
-            m[3] = mask_of(o[4] - o[3], lab.w);
-            reinterpret_cast<typename MaskVec4<MaskT>::T*>(cmask)[gi] = MaskVec4<MaskT>::pack(m);
-        }
-        for (int u = 0; u < q.k; ++u) {
-            const unsigned c = ((m[0] >> u) & 1u) + ((m[1] >> u) & 1u) + ((m[2] >> u) & 1u) + ((m[3] >> u) & 1u);
-            const unsigned w = __reduce_add_sync(0xffffffffu, c);
-            if (lane == u) mine += w;
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+            const int64_t gi = g0 + j * stride + threadIdx.x;
+            const bool live = gi < nvec;
+            const int64_t nxt = __shfl_down_sync(0xffffffffu, A[j].x, 1);
+            const int64_t o4 = (lane == 31 || gi + 1 >= nvec) ? last[j] : nxt;
+            uint32_t m[4] = {0, 0, 0, 0};
+            if (live) {
+                m[0] = mask_of(A[j].y - A[j].x, lab[j].x);
+                m[1] = mask_of(Bq[j].x - A[j].y, lab[j].y);
+                m[2] = mask_of(Bq[j].y - Bq[j].x, lab[j].z);
+                m[3] = mask_of(o4 - Bq[j].y, lab[j].w);
+                reinterpret_cast<typename MaskVec4<MaskT>::T*>(cmask)[gi] = MaskVec4<MaskT>::pack(m);
+            }
+            for (int u = 0; u < q.k; ++u) {
+                const unsigned c = ((m[0] >> u) & 1u) + ((m[1] >> u) & 1u) + ((m[2] >> u) & 1u) + ((m[3] >> u) & 1u);
+                const unsigned w = __reduce_add_sync(0xffffffffu, c);
+                if (lane == u) mine += w;
+            }
         }
     }
     // the last n % 4 vertices
@@ -117,8 +133,8 @@ __global__ void __launch_bounds__(kThreads) k_filter(const int64_t* __restrict__
 
 void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigned long long* counts,
                    cudaStream_t s) {
-    // one group of 4 vertices per thread per pass; grid = SMs x resident blocks (8 x 256 threads)
-    const int grid = grid_for((g.n + 3) / 4, kThreads, 148 * 8);
+    // 4 groups of 4 vertices per thread per pass; grid = SMs x resident blocks (8 x 256 threads)
+    const int grid = grid_for((g.n + 15) / 16, kThreads, 148 * 8);
     switch (mask_bytes_for(q.k)) {
         case 1: k_filter<uint8_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint8_t*)cmask, counts); break;
         case 2: k_filter<uint16_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint16_t*)cmask, counts); break;

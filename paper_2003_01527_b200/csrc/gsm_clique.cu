@@ -287,7 +287,7 @@ __host__ __device__ inline int64_t tri_words(int d) {
 }
 
 struct CtaLay {
-    int64_t h, tb, s, rl, rh, rb, A;  // offsets (int32 units) in shared memory or the slab
+    int64_t h, tb, s, rl, rh, rw, rb, A;  // offsets (int32 units) in shared memory or the slab
     int64_t smem_ints, slab_ints;
 };
 
@@ -307,6 +307,8 @@ __host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool has
     q += dmax;
     L.rh = q;
     q += dmax;
+    L.rw = q;  // K4: nonzero word range of each bit row, lo << 16 | hi (hi exclusive)
+    q += K == 4 ? dmax : 0;
     q = (q + 1) & ~1LL;  // int64 alignment
     L.rb = q;
     q += 2 * (int64_t)dmax;
@@ -335,6 +337,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     int32_t* S = ws + L.s;
     int32_t* RL = ws + L.rl;
     int32_t* RH = ws + L.rh;  // nh_off of each S entry (-1: no hashed N+)
+    int32_t* RW = ws + L.rw;  // K4: nonzero word range [lo, hi) of bit row i, lo << 16 | hi
     int64_t* RB = reinterpret_cast<int64_t*>(ws + L.rb);
     unsigned* A = reinterpret_cast<unsigned*>(ws + L.A);
     unsigned long long cnt = 0, items = 0, words = 0, sent = 0;
@@ -569,6 +572,23 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         }
         if (K == 3) continue;
         __syncthreads();
+        // nonzero word range of every bit row (level 3 intersects only the overlap of two
+        // rows' ranges instead of every word from j/32 to the end)
+        for (int i = wib; i < d; i += NW) {
+            const int w0 = i >> 5;
+            const unsigned* Ai = A + TB[w0] + (i & 31) * TB[W + 1 + w0] - w0;
+            int lo = W, hi = w0;
+            for (int base = w0; base < W; base += 32) {
+                const int w = base + lane;
+                const unsigned nz = __ballot_sync(kFull, w < W && Ai[w] != 0u);
+                if (nz) {
+                    if (lo == W) lo = base + __ffs(nz) - 1;
+                    hi = base + 32 - __clz(nz);
+                }
+            }
+            if (lane == 0) RW[i] = lo < hi ? (lo << 16) | hi : 0;
+        }
+        __syncthreads();
         // ---- level 3: for every level-2 partial result (u, S[i], S[j]) (bit j of A[i]):
         //      |{l : A[i] bit l and A[j] bit l}| = popc over words of A[i] & A[j]
         // (i, j) pairs are queued per warp across rows (sJ[.][0..31] = j, [32..63] = i) and
@@ -582,10 +602,13 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int wi = i >> 5, wj = j >> 5;
                     const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
                     const unsigned* Aj = A + TB[wj] + (j & 31) * TB[W + 1 + wj] - wj;
+                    const unsigned ri = (unsigned)RW[i], rj = (unsigned)RW[j];
+                    const int x0 = max(wj, (int)max(ri >> 16, rj >> 16));
+                    const int x1 = (int)min(ri & 0xffffu, rj & 0xffffu);
                     unsigned c = 0;
-                    for (int x = wj; x < W; ++x) c += __popc(Ai[x] & Aj[x]);
+                    for (int x = x0; x < x1; ++x) c += __popc(Ai[x] & Aj[x]);
                     cnt += c;
-                    words += W - wj;
+                    words += x1 > x0 ? x1 - x0 : 0;
                 }
                 __syncwarp();
             };
@@ -596,7 +619,8 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 if (i >= d - 1) break;
                 const int wi = i >> 5;
                 const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
-                for (int w = wi; w < W; ++w) {
+                const unsigned ri = (unsigned)RW[i];
+                for (int w = max(wi, (int)(ri >> 16)); w < (int)(ri & 0xffffu); ++w) {
                     unsigned bits = Ai[w];
                     while (bits) {
                         const int take = min(__popc(bits), 32 - nJ);

@@ -67,6 +67,12 @@ struct DevGraph {
     // re-sorted by (label(w), w), stored as keys label(w) << idbits | w, same offsets
     int32_t* lkeys = nullptr;
     int32_t idbits = 0;
+    // label index of the keyed lists (vertices with degree >= lidx_min, labels <= 63): lidx_off[v]
+    // = first entry of v's (max_label + 2) int32 offsets (relative to off[v]) where each label's
+    // segment starts, or -1 — a plan row's label segment is two loads instead of two binary
+    // searches over the whole list
+    int32_t* lidx_off = nullptr;
+    int32_t* lidx = nullptr;
     uint32_t max_label = 0;
     int32_t* new2old = nullptr;   // n
     int32_t* old2new = nullptr;   // n
@@ -207,6 +213,7 @@ struct Knobs {
     int hub_bits = 65536;     // GSM_HUB_BITS: H of the hub adjacency bitmap built at load (0 = none; R-MAT-24: 32k 378, 64k 364 ms)
     int clique_hub = 1;       // GSM_CLIQUE_HUB: clique rows of a hub pivot by bitmap lookups
     int clique_hub_ratio = 64;  // GSM_CLIQUE_HUB_RATIO: lookups when 32 nj <= ratio |N+(S[i])|
+    int lidx_min = 32;        // GSM_LIDX_MIN (read at gsm_load_graph): label index for degree >= this (0 = none)
     int nhash_min = 16;       // GSM_NHASH_MIN (read at gsm_load_graph): hashed N+(v) for |N+(v)| >= this (0 = none)
     int clique_nh_stream = 64;  // GSM_CLIQUE_NH_STREAM: with a table, stream N+(S[i]) when 32 len <= this x nj
     int order = 0;            // GSM_ORDER (read at gsm_load_graph): 0 = rank by (degree, id), 1 = approximate degeneracy

@@ -79,6 +79,7 @@ void load_knobs() {
     k.clique_hub_ratio = env_or("GSM_CLIQUE_HUB_RATIO", k.clique_hub_ratio);
     k.order = env_or("GSM_ORDER", k.order);
     k.nhash_min = std::max(0, env_or("GSM_NHASH_MIN", k.nhash_min));
+    k.lidx_min = std::max(0, env_or("GSM_LIDX_MIN", k.lidx_min));
     k.clique_nh_stream = env_or("GSM_CLIQUE_NH_STREAM", k.clique_nh_stream);
     g_knobs = k;
 }
@@ -379,6 +380,37 @@ __global__ void k_nh_insert(const int64_t* __restrict__ off, const int32_t* __re
     }
 }
 
+// label index: per indexed vertex, nl + 1 relative offsets (segment starts of labels 0..nl-1, then
+// the list length); warp per vertex, lanes over labels, each a binary search in the keyed list
+__global__ void k_lidx_sizes(const int64_t* __restrict__ off, int64_t n, int lmin, int nl, int64_t* __restrict__ sz) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        sz[v] = off[v + 1] - off[v] >= lmin ? nl + 1 : 0;
+}
+
+__global__ void k_lidx_build(const int64_t* __restrict__ off, const int32_t* __restrict__ lkeys,
+                             const int64_t* __restrict__ sz, const int64_t* __restrict__ excl, int64_t n, int nl,
+                             int idbits, int32_t* __restrict__ lidx_off, int32_t* __restrict__ lidx) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n; v += nw) {
+        if (sz[v] == 0) {
+            if (lane == 0) lidx_off[v] = -1;
+            continue;
+        }
+        const int64_t b = off[v], e = off[v + 1];
+        if (lane == 0) lidx_off[v] = (int32_t)excl[v];
+        for (int l = lane; l <= nl; l += 32) {
+            int64_t lo = b, hi = e;
+            const int64_t key = (int64_t)l << idbits;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int64_t)lkeys[mid] < key) lo = mid + 1; else hi = mid;
+            }
+            lidx[excl[v] + l] = (int32_t)(lo - b);
+        }
+    }
+}
+
 __global__ void k_nplus(const int64_t* __restrict__ off, const int32_t* __restrict__ up,
                         const int32_t* __restrict__ nh_off, int64_t n, int4* __restrict__ np) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
@@ -443,7 +475,8 @@ static void free_graph(gsm_graph* h) {
     // graph arrays come from the device's stream-ordered pool (kept cached by its release
     // threshold, so a load/free/load cycle does not re-map memory)
     for (void* p : {(void*)g.off, (void*)g.cols, (void*)g.up, (void*)g.labels, (void*)g.lkeys, (void*)g.new2old,
-                    (void*)g.old2new, (void*)g.hub_bits, (void*)g.nh_off, (void*)g.nh_tab, (void*)g.nplus})
+                    (void*)g.old2new, (void*)g.hub_bits, (void*)g.nh_off, (void*)g.nh_tab, (void*)g.nplus,
+                    (void*)g.lidx_off, (void*)g.lidx})
         if (p) cudaFreeAsync(p, h->stream);
     cudaStreamSynchronize(h->stream);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -683,6 +716,30 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
             GSM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, ekeys.p, esorted.p, nnz, 0, end_bit, s));
             k_extract_cols<<<grid_for(nnz), 256, 0, s>>>(esorted.p, nnz, g.lkeys);
             GSM_LAUNCH("k_extract_cols(lkeys)");
+            const int nl = (int)hmax + 1;
+            if (knobs().lidx_min > 0 && nl <= 64) {
+                DevBuf<int64_t> sz, excl;
+                sz.ensure(n, s);
+                excl.ensure(n + 1, s);
+                k_lidx_sizes<<<grid_for(n), 256, 0, s>>>(g.off, n, knobs().lidx_min, nl, sz.p);
+                GSM_LAUNCH("k_lidx_sizes");
+                GSM_CUDA(cudaMemsetAsync(excl.p, 0, sizeof(int64_t), s));
+                size_t sb = 0;
+                GSM_CUDA(cub::DeviceScan::InclusiveSum(nullptr, sb, sz.p, excl.p + 1, n, s));
+                DevBuf<uint8_t> stmp;
+                stmp.ensure(sb, s);
+                GSM_CUDA(cub::DeviceScan::InclusiveSum(stmp.p, sb, sz.p, excl.p + 1, n, s));
+                int64_t total = 0;
+                GSM_CUDA(cudaMemcpyAsync(&total, excl.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+                GSM_CUDA(cudaStreamSynchronize(s));
+                if (total > 0 && total < (int64_t)INT32_MAX) {
+                    g.lidx_off = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
+                    g.lidx = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * total, s));
+                    k_lidx_build<<<grid_for(n * 32), 256, 0, s>>>(g.off, g.lkeys, sz.p, excl.p, n, nl, idbits,
+                                                                  g.lidx_off, g.lidx);
+                    GSM_LAUNCH("k_lidx_build");
+                }
+            }
         }
     }
     GSM_CUDA(cudaStreamSynchronize(s));

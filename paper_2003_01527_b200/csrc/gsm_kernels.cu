@@ -486,7 +486,9 @@ __global__ void __launch_bounds__(kThreads) k_plan_rows(const Frontier F, int64_
                                                         const int32_t* __restrict__ up, int64_t n,
                                                         int64_t* __restrict__ rbeg, int64_t* __restrict__ rlen,
                                                         uint8_t* __restrict__ rpiv, int64_t* __restrict__ cbeg,
-                                                        int32_t* __restrict__ clen) {
+                                                        int32_t* __restrict__ clen,
+                                                        const int32_t* __restrict__ lidx_off,
+                                                        const int32_t* __restrict__ lidx) {
     const int nb = L.nb;
     int32_t buf[kMaxK];
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R; r += (int64_t)gridDim.x * blockDim.x) {
@@ -505,8 +507,18 @@ __global__ void __launch_bounds__(kThreads) k_plan_rows(const Frontier F, int64_
                 const int32_t a = row[L.bpos[q]];
                 int64_t s0 = off[a], t0 = off[a + 1];
                 if (!empty) {
-                    s0 = lower_bound_cols(cols, s0, t0, klo);
-                    t0 = lower_bound_cols(cols, s0, t0, khi);
+                    const int32_t li = lidx_off ? __ldg(lidx_off + a) : -1;
+                    if (li >= 0) {  // label segment from the index, ID bounds searched inside it
+                        const int lab = (int)((uint32_t)L.key_base >> __popc(L.idmask));
+                        const int64_t b = s0;
+                        s0 = b + __ldg(lidx + li + lab);
+                        t0 = b + __ldg(lidx + li + lab + 1);
+                        if (lov >= 0) s0 = lower_bound_cols(cols, s0, t0, klo);
+                        if (hiv < n) t0 = lower_bound_cols(cols, s0, t0, khi);
+                    } else {
+                        s0 = lower_bound_cols(cols, s0, t0, klo);
+                        t0 = lower_bound_cols(cols, s0, t0, khi);
+                    }
                 } else {
                     t0 = s0;
                 }
@@ -627,7 +639,8 @@ void launch_plan_rows(const DevGraph& g, const Frontier& F, int64_t R, const Lev
         GSM_LAUNCH("k_plan_rows_grp");
         return;
     }
-    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, cols, g.up, g.n, rbeg, rlen, rpiv, cbeg, clen);
+    k_plan_rows<<<grid_for(R), kThreads, 0, s>>>(F, R, L, g.off, cols, g.up, g.n, rbeg, rlen, rpiv, cbeg, clen,
+                                                 L.keyed ? g.lidx_off : nullptr, g.lidx);
     GSM_LAUNCH("k_plan_rows");
 }
 

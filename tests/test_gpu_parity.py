@@ -207,7 +207,7 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
         G.free()
 
 
-@pytest.mark.parametrize("pair", ["1", "warp", "0", "plan_groups", "nohub", "swap1", "swap1_warp"])
+@pytest.mark.parametrize("pair", ["1", "warp", "0", "plan_groups", "nohub", "swap1", "swap1_warp", "nolidx", "lidx_all"])
 def test_pair_tail(pair, monkeypatch):
     """COUNT mode with the last two positions an independent pair (k_pair: |Cp||Cq| - |Cp∩Cq|)
     against the oracle's count, labeled and unlabeled, with and without symmetry; "0" =
@@ -215,6 +215,12 @@ def test_pair_tail(pair, monkeypatch):
     the warp-per-row kernel (no thread-per-row pass)."""
     if pair == "plan_groups":  # row plans by lane groups instead of one thread per row (the default)
         monkeypatch.setenv("GSM_PLAN_GROUPS", "1")
+    # label index of the keyed lists (read at load): "nolidx" = binary searches for every label
+    # segment, "lidx_all" = every vertex indexed
+    if pair == "nolidx":
+        monkeypatch.setenv("GSM_LIDX_MIN", "0")
+    if pair == "lidx_all":
+        monkeypatch.setenv("GSM_LIDX_MIN", "1")
     # membership tests: these small graphs are all hubs by default (bitmap tests); "nohub" = binary
     # searches only; "swap1" = search the image in N(v) whenever v's list is the shorter one
     if pair in ("nohub", "swap1", "swap1_warp"):

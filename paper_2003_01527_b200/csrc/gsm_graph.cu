@@ -411,6 +411,33 @@ __global__ void k_lidx_build(const int64_t* __restrict__ off, const int32_t* __r
     }
 }
 
+// number of trailing vertices (new order) with degree >= big, and where their lists start;
+// degrees are non-decreasing in the (degree, id) order, so they form a suffix
+__global__ void k_big_suffix(const int64_t* __restrict__ off, int64_t n, int64_t big, int64_t* out) {
+    // the first vertex with degree >= big: a binary search by one thread (log2 n steps)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (off[mid + 1] - off[mid] < big) lo = mid + 1; else hi = mid;
+        }
+        out[0] = n - lo;
+        out[1] = off[lo];
+    }
+}
+
+// warp per long list: (list index << 32 | id) keys of its entries
+__global__ void k_big_keys(const int64_t* __restrict__ off, const int32_t* __restrict__ ecols, int64_t first,
+                           int64_t nbig, int64_t base, uint64_t* __restrict__ keys) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; b < nbig; b += nw) {
+        const int64_t v = first + b;
+        for (int64_t x = off[v] + lane; x < off[v + 1]; x += 32)
+            keys[x - base] = ((uint64_t)b << 32) | (uint32_t)ecols[x];
+    }
+}
+
 __global__ void k_nplus(const int64_t* __restrict__ off, const int32_t* __restrict__ up,
                         const int32_t* __restrict__ nh_off, int64_t n, int4* __restrict__ np) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
@@ -629,11 +656,50 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         ecols.ensure(nnz, s);
         k_edge_cols<<<grid_for(n * 32), 256, 0, s>>>(d_off, d_cols, g.off, g.new2old, g.old2new, n, ecols.p);
         GSM_LAUNCH("k_edge_cols");
-        size_t tmp_bytes = 0;
-        GSM_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, ecols.p, g.cols, nnz, n, g.off, g.off + 1, s));
-        DevBuf<uint8_t> tmp;
-        tmp.ensure(tmp_bytes, s);
-        GSM_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.p, tmp_bytes, ecols.p, g.cols, nnz, n, g.off, g.off + 1, s));
+        // Under the (degree, id) order the long lists are the last ranks.  CUB's segmented sort
+        // runs few, long segments at low occupancy (ncu: 43 ms, 12.5 % warps active on
+        // R-MAT-24), so the lists of degree >= kBig are sorted together by one radix sort of
+        // (list index, id) keys and only the prefix of short lists goes through the
+        // segmented sort.
+        constexpr int64_t kBig = 8192;
+        int64_t nbig = 0, split = nnz;
+        if (knobs().order == 0 && g.max_degree >= kBig) {
+            DevBuf<int64_t> hv;
+            hv.ensure(2, s);
+            k_big_suffix<<<grid_for(n), 256, 0, s>>>(g.off, n, kBig, hv.p);
+            GSM_LAUNCH("k_big_suffix");
+            int64_t h[2];
+            GSM_CUDA(cudaMemcpyAsync(h, hv.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+            GSM_CUDA(cudaStreamSynchronize(s));
+            nbig = h[0];
+            split = h[1];
+        }
+        const int64_t nsmall = n - nbig;
+        if (split > 0) {
+            size_t tmp_bytes = 0;
+            GSM_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, ecols.p, g.cols, split, nsmall, g.off,
+                                                        g.off + 1, s));
+            DevBuf<uint8_t> tmp;
+            tmp.ensure(tmp_bytes, s);
+            GSM_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.p, tmp_bytes, ecols.p, g.cols, split, nsmall, g.off,
+                                                        g.off + 1, s));
+        }
+        if (nbig > 0) {
+            const int64_t E = nnz - split;
+            DevBuf<uint64_t> bk, bs;
+            bk.ensure(E, s);
+            bs.ensure(E, s);
+            k_big_keys<<<grid_for(nbig * 32), 256, 0, s>>>(g.off, ecols.p, nsmall, nbig, split, bk.p);
+            GSM_LAUNCH("k_big_keys");
+            const int end_bit = 32 + bits_for((uint64_t)nbig);
+            size_t tb = 0;
+            GSM_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, bk.p, bs.p, E, 0, end_bit, s));
+            DevBuf<uint8_t> tmp;
+            tmp.ensure(tb, s);
+            GSM_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, bk.p, bs.p, E, 0, end_bit, s));
+            k_extract_cols<<<grid_for(E), 256, 0, s>>>(bs.p, E, g.cols + split);
+            GSM_LAUNCH("k_extract_cols(big)");
+        }
     }
     k_up<<<grid_for(n), 256, 0, s>>>(g.off, g.cols, n, g.up);
     GSM_LAUNCH("k_up");

@@ -724,3 +724,28 @@ def test_merge_rows():
         tb = torch.from_numpy(b).cuda().reshape(nb, w)
         out = gsm.gsm_merge_rows(ta, tb).cpu().numpy()
         assert_rows_equal(out, oracle.sort_rows(np.concatenate([a, b]).reshape(-1, w)), f"merge w={w} {na}+{nb}")
+
+
+def test_long_lists_relabel():
+    """gsm_load_graph sorts the relabelled lists of degree >= 8192 by one radix sort of (list,
+    id) keys instead of the segmented sort: a hub of degree 12,000 plus a second one of 9,000
+    over random edges — K3 / P3 / C4 counts and K3 rows equal the oracle's."""
+    rng = np.random.default_rng(21)
+    n = 12500
+    src = [np.zeros(12000, np.int64), np.ones(9000, np.int64)]
+    dst = [np.arange(1, 12001), np.arange(2, 9002)]
+    e = rng.integers(2, n, size=(30000, 2))
+    src.append(e[:, 0])
+    dst.append(e[:, 1])
+    g = gi.csr_from_edges(n, np.concatenate(src), np.concatenate(dst))
+    G = load(g)
+    try:
+        for qn in ["K3", "P3", "C4"]:
+            q = gi.query(qn)
+            cnt, ref = oracle.match(g, q, count_only=qn != "K3")
+            c, rows, _ = run(G, q, "enumerate" if qn == "K3" else "count")
+            assert c == cnt, (qn, c, cnt)
+            if qn == "K3":
+                assert_rows_equal(rows, ref, "hub K3")
+    finally:
+        G.free()

@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     unsigned long long cnt = 0, items = 0, words = 0, sent = 0;
     unsigned probes = 0;
     unsigned long long cy[4] = {0, 0, 0, 0};
+    unsigned long long pi[4] = {0, 0, 0, 0};  // GSM_TRACE=2: keys / entries per row strategy
     long long tc = 0;
     for (;;) {
         if (a.cyc) tc = clock64();
@@ -470,6 +471,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                         f = (__ldg(hr + (c >> 5)) >> (c & 31)) & 1u;
                     }
                     items += live;
+                    if (a.cyc) pi[0] += live;
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
                         if (lane == 0) Ai[w] = bits;
@@ -493,6 +495,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int j = (w << 5) + lane;
                     const bool live = j > i && j < d;
                     items += live;
+                    if (a.cyc) pi[1] += live;
                     const bool f = live && nh_find(a.nh_tab, tb, B, S[j], probes);
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
@@ -521,6 +524,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int32_t v1 = x + 32 < le ? cols[x + 32] : INT32_MAX;
                     if (!__any_sync(kFull, v0 <= smax)) break;
                     if (lane == 0) items += min((int64_t)64, le - x0);
+                    if (a.cyc && lane == 0) pi[2] += min((int64_t)64, le - x0);
                     const int j0 = K == 4 ? ck_find(Tk, Tk + 2 * P, P, seed, v0) : (ck_has(Tk, P, seed, v0) ? 0 : -1);
                     const int j1 = K == 4 ? ck_find(Tk, Tk + 2 * P, P, seed, v1) : (ck_has(Tk, P, seed, v1) ? 0 : -1);
                     if (K == 4) {
@@ -545,6 +549,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int j = (w << 5) + lane;
                     const bool live = j > i && j < d;
                     items += live;
+                    if (a.cyc) pi[3] += live;
                     const int32_t key = live ? S[j] : INT32_MAX;
                     int lo = 0, hi = 32;  // last slice whose first entry <= key
 #pragma unroll
@@ -645,8 +650,15 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         }
         if (a.cyc) cy[3] += clock64() - tc;
     }
-    if (a.cyc && lane == 0)
-        for (int q = 0; q < 4; ++q) atomicAdd(&a.cyc[q], cy[q]);
+    if (a.cyc) {
+        for (int q = 0; q < 4; ++q)
+            for (int o = 16; o; o >>= 1) pi[q] += __shfl_xor_sync(kFull, pi[q], o);
+        if (lane == 0)
+            for (int q = 0; q < 4; ++q) {
+                atomicAdd(&a.cyc[q], cy[q]);
+                atomicAdd(&a.cyc[4 + q], pi[q]);
+            }
+    }
     unsigned long long pr = probes;
     for (int o = 16; o; o >>= 1) {
         cnt += __shfl_xor_sync(kFull, cnt, o);
@@ -801,8 +813,8 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     DevBuf<unsigned long long> cyc;
     a.cyc = nullptr;
     if (knobs().trace == 2) {
-        cyc.ensure(4, s);
-        GSM_CUDA(cudaMemsetAsync(cyc.p, 0, 4 * sizeof(unsigned long long), s));
+        cyc.ensure(8, s);
+        GSM_CUDA(cudaMemsetAsync(cyc.p, 0, 8 * sizeof(unsigned long long), s));
         a.cyc = cyc.p;
     }
     a.slab = nullptr;
@@ -858,13 +870,16 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
         }
     }
     if (a.cyc) {
-        unsigned long long hc[4];
+        unsigned long long hc[8];
         GSM_CUDA(cudaMemcpyAsync(hc, a.cyc, sizeof(hc), cudaMemcpyDeviceToHost, s));
         GSM_CUDA(cudaStreamSynchronize(s));
         const double t = (double)(hc[0] + hc[1] + hc[2] + hc[3]) + 1e-9;
         std::fprintf(stderr, "[gsm clique K%d] k_clique_cta warp-cycles: setup %.1f%%  stream rows %.1f%%  search rows %.1f%%"
                      "  level 3 %.1f%%  (total %.3g)\n", K, 100 * hc[0] / t, 100 * hc[1] / t, 100 * hc[2] / t,
                      100 * hc[3] / t, t);
+        std::fprintf(stderr, "[gsm clique K%d] k_clique_cta row keys/entries: hub bitmap %.3g  hashed N+ %.3g  "
+                     "streamed %.3g  binary search %.3g\n", K, (double)hc[4], (double)hc[5], (double)hc[6],
+                     (double)hc[7]);
     }
     return launches;
 }

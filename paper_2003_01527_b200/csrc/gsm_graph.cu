@@ -516,6 +516,15 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
     if (!out) fail(GSM_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     load_knobs();
+    // GSM_TRACE=1: per-phase load times (a stream sync after each phase; tracing only)
+    auto tph = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {
+        if (knobs().trace != 1) return;
+        cudaStreamSynchronize(s);
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[gsm load] %-26s %8.2f ms\n", name, std::chrono::duration<double, std::milli>(t - tph).count());
+        tph = t;
+    };
     if (opts && opts->struct_size != sizeof(gsm_load_opts)) fail(GSM_ERR_INVALID_ARGUMENT, "gsm_load_opts.struct_size mismatch");
     if (n <= 0) fail(GSM_ERR_INVALID_GRAPH, "graph has no vertices");
     if (n >= (int64_t)0x7fffffff) fail(GSM_ERR_INVALID_GRAPH, "more than 2^31-1 vertices");
@@ -600,6 +609,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
     g.new2old = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
     g.old2new = static_cast<int32_t*>(dev_alloc(sizeof(int32_t) * n, s));
 
+    phase("upload + validate");
     // 1. rank by (degree, id) (GSM_ORDER=1: by (peeling round, degree, id), k_adg_*)
     {
         DevBuf<uint64_t> keys, sorted;
@@ -635,6 +645,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         stmp.ensure(sb, s);
         GSM_CUDA(cub::DeviceScan::InclusiveSum(stmp.p, sb, newdeg.p, g.off + 1, n, s));
     }
+    phase("rank + offsets");
     // 2. relabelled lists, each re-sorted (segmented sort of 32-bit ids: the rows are
     //    already in their new order, only the ids inside a list move)
     if (nnz > 0 && nnz > (int64_t)INT32_MAX) {  // beyond 32-bit segmented-sort sizes: (row, id) keys
@@ -703,6 +714,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
     }
     k_up<<<grid_for(n), 256, 0, s>>>(g.off, g.cols, n, g.up);
     GSM_LAUNCH("k_up");
+    phase("relabelled lists");
     // 3. hub adjacency bitmap of the H highest-ranked vertices (load-time derived data)
     if (knobs().hub_bits > 0) {
         const int32_t H = (int32_t)std::min<int64_t>(n, knobs().hub_bits) & ~31;
@@ -717,6 +729,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
             GSM_LAUNCH("k_hub_bits");
         }
     }
+    phase("hub bitmap");
     // 4. hashed N+(v) tables of the vertices with |N+(v)| >= nh_min (load-time derived data)
     if (knobs().nhash_min > 0 && nnz > 0) {
         DevBuf<int64_t> nb, excl;
@@ -745,9 +758,11 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
             GSM_LAUNCH("k_nh_insert");
         }
     }
+    phase("hashed N+ tables");
     g.nplus = static_cast<int4*>(dev_alloc(sizeof(int4) * n, s));
     k_nplus<<<grid_for(n), 256, 0, s>>>(g.off, g.up, g.nh_off, n, g.nplus);
     GSM_LAUNCH("k_nplus");
+    phase("N+ descriptors");
     if (labels) {
         g.labels = static_cast<uint32_t*>(dev_alloc(sizeof(uint32_t) * n, s));
         k_permute_labels<<<grid_for(n), 256, 0, s>>>(d_lab, g.new2old, n, g.labels);
@@ -808,6 +823,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
             }
         }
     }
+    phase("labels + keyed lists");
     GSM_CUDA(cudaStreamSynchronize(s));
     *out = h.release();
 }

@@ -10,3 +10,4 @@ b r22_nolidx GSM_LIDX_MIN=0 python bench.py --workload rmat22 --steps 5 --warmup
 b r22_lidx8 GSM_LIDX_MIN=8 python bench.py --workload rmat22 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0
 b r16 python bench.py --workload rmat16 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0
 echo perf3-done
+timeout 600 python tools/load_phases.py rmat24 rmat22 > gpurun_out/load_phases.log 2>&1; cat gpurun_out/load_phases.log | tail -40

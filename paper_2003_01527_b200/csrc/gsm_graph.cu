@@ -518,9 +518,11 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
     load_knobs();
     // GSM_TRACE=1: per-phase load times (a stream sync after each phase; tracing only)
     auto tph = std::chrono::steady_clock::now();
+    cudaStream_t stream_for_trace = nullptr;
+    cudaStream_t* out_stream = &stream_for_trace;
     auto phase = [&](const char* name) {
-        if (knobs().trace != 1) return;
-        cudaStreamSynchronize(s);
+        if (knobs().trace != 1 || !*out_stream) return;
+        cudaStreamSynchronize(*out_stream);
         const auto t = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[gsm load] %-26s %8.2f ms\n", name, std::chrono::duration<double, std::milli>(t - tph).count());
         tph = t;
@@ -548,6 +550,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         h->own_stream = true;
     }
     cudaStream_t s = h->stream;
+    stream_for_trace = s;
     // keep freed pool memory cached between matches
     cudaMemPool_t pool;
     GSM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

@@ -340,10 +340,17 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     int32_t* RW = ws + L.rw;  // K4: nonzero word range [lo, hi) of bit row i, lo << 16 | hi
     int64_t* RB = reinterpret_cast<int64_t*>(ws + L.rb);
     unsigned* A = reinterpret_cast<unsigned*>(ws + L.A);
-    unsigned long long cnt = 0, items = 0, words = 0, sent = 0;
+    unsigned long long cnt = 0;
+    unsigned items = 0, words = 0, sent = 0;  // per-thread stats (32-bit: fewer registers)
     unsigned probes = 0;
-    unsigned long long cy[4] = {0, 0, 0, 0};
-    unsigned long long pi[4] = {0, 0, 0, 0};  // GSM_TRACE=2: keys / entries per row strategy
+    // GSM_TRACE=2 (a.cyc): phase cycles and keys per row strategy go straight to global
+    // counters from lane 0 — nothing held in registers across the kernel when tracing is off
+    auto trace = [&](int slot, long long cycles, unsigned long long keys, int kslot) {
+        if (lane == 0) {
+            atomicAdd(&a.cyc[slot], (unsigned long long)cycles);
+            if (kslot >= 0) atomicAdd(&a.cyc[kslot], keys);
+        }
+    };
     long long tc = 0;
     for (;;) {
         if (a.cyc) tc = clock64();
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         const int32_t smax = S[d - 1];
         if (a.cyc) {
             const long long t1 = clock64();
-            cy[0] += t1 - tc;
+            trace(0, t1 - tc, 0, -1);
             tc = t1;
         }
         // ---- rows A[i] (level 1 -> 2 connection tests), warps take rows dynamically
@@ -471,7 +478,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                         f = (__ldg(hr + (c >> 5)) >> (c & 31)) & 1u;
                     }
                     items += live;
-                    if (a.cyc) pi[0] += live;
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
                         if (lane == 0) Ai[w] = bits;
@@ -481,7 +487,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 }
                 if (a.cyc) {
                     const long long t1 = clock64();
-                    cy[2] += t1 - tc;
+                    trace(2, t1 - tc, nj, 4);
                     tc = t1;
                 }
                 continue;
@@ -495,7 +501,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int j = (w << 5) + lane;
                     const bool live = j > i && j < d;
                     items += live;
-                    if (a.cyc) pi[1] += live;
                     const bool f = live && nh_find(a.nh_tab, tb, B, S[j], probes);
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 }
                 if (a.cyc) {
                     const long long t1 = clock64();
-                    cy[2] += t1 - tc;
+                    trace(2, t1 - tc, nj, 5);
                     tc = t1;
                 }
                 continue;
@@ -524,7 +529,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int32_t v1 = x + 32 < le ? cols[x + 32] : INT32_MAX;
                     if (!__any_sync(kFull, v0 <= smax)) break;
                     if (lane == 0) items += min((int64_t)64, le - x0);
-                    if (a.cyc && lane == 0) pi[2] += min((int64_t)64, le - x0);
                     const int j0 = K == 4 ? ck_find(Tk, Tk + 2 * P, P, seed, v0) : (ck_has(Tk, P, seed, v0) ? 0 : -1);
                     const int j1 = K == 4 ? ck_find(Tk, Tk + 2 * P, P, seed, v1) : (ck_has(Tk, P, seed, v1) ? 0 : -1);
                     if (K == 4) {
@@ -536,7 +540,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 }
                 if (a.cyc) {
                     const long long t1 = clock64();
-                    cy[1] += t1 - tc;
+                    trace(1, t1 - tc, len, 6);
                     tc = t1;
                 }
             } else {
@@ -549,7 +553,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int j = (w << 5) + lane;
                     const bool live = j > i && j < d;
                     items += live;
-                    if (a.cyc) pi[3] += live;
                     const int32_t key = live ? S[j] : INT32_MAX;
                     int lo = 0, hi = 32;  // last slice whose first entry <= key
 #pragma unroll
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 }
                 if (a.cyc) {
                     const long long t1 = clock64();
-                    cy[2] += t1 - tc;
+                    trace(2, t1 - tc, nj, 7);
                     tc = t1;
                 }
             }
@@ -648,33 +651,24 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             }
             if (nJ > 0) flush(nJ);
         }
-        if (a.cyc) cy[3] += clock64() - tc;
+        if (a.cyc) trace(3, clock64() - tc, 0, -1);
     }
-    if (a.cyc) {
-        for (int q = 0; q < 4; ++q)
-            for (int o = 16; o; o >>= 1) pi[q] += __shfl_xor_sync(kFull, pi[q], o);
-        if (lane == 0)
-            for (int q = 0; q < 4; ++q) {
-                atomicAdd(&a.cyc[q], cy[q]);
-                atomicAdd(&a.cyc[4 + q], pi[q]);
-            }
-    }
-    unsigned long long pr = probes;
+    unsigned long long pr = probes, it = items, wd = words;
     for (int o = 16; o; o >>= 1) {
         cnt += __shfl_xor_sync(kFull, cnt, o);
-        items += __shfl_xor_sync(kFull, items, o);
+        it += __shfl_xor_sync(kFull, it, o);
         pr += __shfl_xor_sync(kFull, pr, o);
-        words += __shfl_xor_sync(kFull, words, o);
+        wd += __shfl_xor_sync(kFull, wd, o);
     }
     if (lane == 0) {
         if (cnt) {
             atomicAdd(a.count, cnt);
             atomicAdd(&a.stats[3], cnt);
         }
-        if (items) atomicAdd(&a.stats[0], items);
+        if (it) atomicAdd(&a.stats[0], it);
         if (pr) atomicAdd(&a.stats[1], pr);
-        if (words) atomicAdd(&a.stats[2], words);
-        if (sent) atomicAdd(&a.stats[4], sent);
+        if (wd) atomicAdd(&a.stats[2], wd);
+        if (sent) atomicAdd(&a.stats[4], (unsigned long long)sent);
     }
 }
 

@@ -213,6 +213,7 @@ struct Knobs {
     int hub_bits = 65536;     // GSM_HUB_BITS: H of the hub adjacency bitmap built at load (0 = none; R-MAT-24: 32k 378, 64k 364 ms)
     int clique_hub = 1;       // GSM_CLIQUE_HUB: clique rows of a hub pivot by bitmap lookups
     int clique_hub_ratio = 64;  // GSM_CLIQUE_HUB_RATIO: lookups when 32 nj <= ratio |N+(S[i])|
+    int filter_u = 2;         // GSM_FILTER_U: K1 groups of 4 vertices per thread per pass (1, 2, 4)
     int lidx_min = 32;        // GSM_LIDX_MIN (read at gsm_load_graph): label index for degree >= this (0 = none)
     int nhash_min = 16;       // GSM_NHASH_MIN (read at gsm_load_graph): hashed N+(v) for |N+(v)| >= this (0 = none)
     int clique_nh_stream = 64;  // GSM_CLIQUE_NH_STREAM: with a table, stream N+(S[i]) when 32 len <= this x nj

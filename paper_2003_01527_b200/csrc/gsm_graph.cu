@@ -80,6 +80,10 @@ void load_knobs() {
     k.order = env_or("GSM_ORDER", k.order);
     k.nhash_min = std::max(0, env_or("GSM_NHASH_MIN", k.nhash_min));
     k.lidx_min = std::max(0, env_or("GSM_LIDX_MIN", k.lidx_min));
+    {
+        const int fu = env_or("GSM_FILTER_U", k.filter_u);
+        k.filter_u = (fu == 1 || fu == 2 || fu == 4) ? fu : 2;
+    }
     k.clique_nh_stream = env_or("GSM_CLIQUE_NH_STREAM", k.clique_nh_stream);
     g_knobs = k;
 }

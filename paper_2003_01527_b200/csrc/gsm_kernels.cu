@@ -57,8 +57,8 @@ struct MaskVec4<uint32_t> {
     __device__ static T pack(const uint32_t* m) { return make_uint4(m[0], m[1], m[2], m[3]); }
 };
 
-template <typename MaskT>
-__global__ void __launch_bounds__(kThreads) k_filter(const int64_t* __restrict__ off,
+template <typename MaskT, int kU>
+__global__ void __launch_bounds__(kThreads, 8 / kU) k_filter(const int64_t* __restrict__ off,
                                                      const uint32_t* __restrict__ labels, int64_t n,
                                                      FilterQuery q, MaskT* __restrict__ cmask,
                                                      unsigned long long* __restrict__ counts) {
@@ -75,7 +75,6 @@ __global__ void __launch_bounds__(kThreads) k_filter(const int64_t* __restrict__
     // use (more bytes in flight per thread: ncu showed the one-group loop at 31 % of DRAM
     // bandwidth, stalled on the shuffle that waits for the offsets); the loop bound is
     // block-uniform so the shuffles stay converged
-    constexpr int kU = 4;
     for (int64_t g0 = (int64_t)blockIdx.x * blockDim.x; g0 < nvec; g0 += stride * kU) {
         longlong2 A[kU], Bq[kU];
         uint4 lab[kU];
@@ -133,12 +132,23 @@ __global__ void __launch_bounds__(kThreads) k_filter(const int64_t* __restrict__
 
 void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigned long long* counts,
                    cudaStream_t s) {
-    // 4 groups of 4 vertices per thread per pass; grid = SMs x resident blocks (8 x 256 threads)
-    const int grid = grid_for((g.n + 15) / 16, kThreads, 148 * 8);
-    switch (mask_bytes_for(q.k)) {
-        case 1: k_filter<uint8_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint8_t*)cmask, counts); break;
-        case 2: k_filter<uint16_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint16_t*)cmask, counts); break;
-        default: k_filter<uint32_t><<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, (uint32_t*)cmask, counts); break;
+    // kU groups of 4 vertices per thread per pass (GSM_FILTER_U = 1, 2, 4); grid = SMs x resident blocks
+    const int U = knobs().filter_u;
+    const int grid = grid_for((g.n + 4 * U - 1) / (4 * U), kThreads, 148 * 8 / U);
+    auto go = [&](auto kern, auto* mask) { kern<<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, mask, counts); };
+    const int mb = mask_bytes_for(q.k);
+    if (U == 4) {
+        if (mb == 1) go(k_filter<uint8_t, 4>, (uint8_t*)cmask);
+        else if (mb == 2) go(k_filter<uint16_t, 4>, (uint16_t*)cmask);
+        else go(k_filter<uint32_t, 4>, (uint32_t*)cmask);
+    } else if (U == 2) {
+        if (mb == 1) go(k_filter<uint8_t, 2>, (uint8_t*)cmask);
+        else if (mb == 2) go(k_filter<uint16_t, 2>, (uint16_t*)cmask);
+        else go(k_filter<uint32_t, 2>, (uint32_t*)cmask);
+    } else {
+        if (mb == 1) go(k_filter<uint8_t, 1>, (uint8_t*)cmask);
+        else if (mb == 2) go(k_filter<uint16_t, 1>, (uint16_t*)cmask);
+        else go(k_filter<uint32_t, 1>, (uint32_t*)cmask);
     }
     GSM_LAUNCH("k_filter");
 }

@@ -149,6 +149,7 @@ struct CliqueArgs {
     const int32_t* nh_off;  // hashed N+(v) tables (DevGraph::nh_*) or nullptr
     const int32_t* nh_tab;
     int32_t nh_stream;      // with a table, a row streams N+(S[i]) only when 32 |N+(S[i])| <= nh_stream x nj
+    int32_t ranges;         // K4: level 3 over the overlap of the rows' nonzero word ranges (else j/32..W)
     int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
     int32_t slab_blocks;    // kGlobal: slabs allocated (the grid must not exceed it)
     unsigned long long* next;   // dynamic root scheduler
@@ -594,6 +595,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     hi = base + 32 - __clz(nz);
                 }
             }
+            if (!a.ranges) lo = w0, hi = W;  // full triangular extent
             if (lane == 0) RW[i] = lo < hi ? (lo << 16) | hi : 0;
         }
         __syncthreads();
@@ -804,6 +806,7 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     a.nh_off = r.nh_off;
     a.nh_tab = r.nh_tab;
     a.nh_stream = knobs().clique_nh_stream;
+    a.ranges = knobs().clique_ranges;
     DevBuf<unsigned long long> cyc;
     a.cyc = nullptr;
     if (knobs().trace == 2) {

@@ -80,9 +80,11 @@ void load_knobs() {
     k.order = env_or("GSM_ORDER", k.order);
     k.nhash_min = std::max(0, env_or("GSM_NHASH_MIN", k.nhash_min));
     k.lidx_min = std::max(0, env_or("GSM_LIDX_MIN", k.lidx_min));
+    k.clique_ranges = env_or("GSM_CLIQUE_RANGES", k.clique_ranges);
+    k.bigsort = env_or("GSM_BIGSORT", k.bigsort);
     {
         const int fu = env_or("GSM_FILTER_U", k.filter_u);
-        k.filter_u = (fu == 1 || fu == 2 || fu == 4) ? fu : 2;
+        k.filter_u = (fu == 1 || fu == 2 || fu == 4) ? fu : 1;
     }
     k.clique_nh_stream = env_or("GSM_CLIQUE_NH_STREAM", k.clique_nh_stream);
     g_knobs = k;
@@ -681,7 +683,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         // segmented sort.
         constexpr int64_t kBig = 8192;
         int64_t nbig = 0, split = nnz;
-        if (knobs().order == 0 && g.max_degree >= kBig) {
+        if (knobs().bigsort && knobs().order == 0 && g.max_degree >= kBig) {
             DevBuf<int64_t> hv;
             hv.ensure(2, s);
             k_big_suffix<<<grid_for(n), 256, 0, s>>>(g.off, n, kBig, hv.p);

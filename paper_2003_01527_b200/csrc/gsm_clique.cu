@@ -593,8 +593,10 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         if (K == 3) continue;
         __syncthreads();
         // nonzero word range of every bit row (level 3 intersects only the overlap of two
-        // rows' ranges instead of every word from j/32 to the end)
-        for (int i = wib; i < d; i += NW) {
+        // rows' ranges instead of every word from j/32 to the end) — for roots with W >= 8
+        // words per row; shorter rows are not worth the extra pass and barrier
+        const bool use_rw = a.ranges && W >= 8;
+        for (int i = wib; use_rw && i < d; i += NW) {
             const int w0 = i >> 5;
             const unsigned* Ai = A + TB[w0] + (i & 31) * TB[W + 1 + w0] - w0;
             int lo = W, hi = w0;
@@ -606,10 +608,9 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     hi = base + 32 - __clz(nz);
                 }
             }
-            if (!a.ranges) lo = w0, hi = W;  // full triangular extent
             if (lane == 0) RW[i] = lo < hi ? (lo << 16) | hi : 0;
         }
-        __syncthreads();
+        if (use_rw) __syncthreads();
         // ---- level 3: for every level-2 partial result (u, S[i], S[j]) (bit j of A[i]):
         //      |{l : A[i] bit l and A[j] bit l}| = popc over words of A[i] & A[j]
         // (i, j) pairs are queued per warp across rows (sJ[.][0..31] = j, [32..63] = i) and
@@ -623,9 +624,12 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const int wi = i >> 5, wj = j >> 5;
                     const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
                     const unsigned* Aj = A + TB[wj] + (j & 31) * TB[W + 1 + wj] - wj;
-                    const unsigned ri = (unsigned)RW[i], rj = (unsigned)RW[j];
-                    const int x0 = max(wj, (int)max(ri >> 16, rj >> 16));
-                    const int x1 = (int)min(ri & 0xffffu, rj & 0xffffu);
+                    int x0 = wj, x1 = W;
+                    if (use_rw) {
+                        const unsigned ri = (unsigned)RW[i], rj = (unsigned)RW[j];
+                        x0 = max(wj, (int)max(ri >> 16, rj >> 16));
+                        x1 = (int)min(ri & 0xffffu, rj & 0xffffu);
+                    }
                     unsigned c = 0;
                     for (int x = x0; x < x1; ++x) c += __popc(Ai[x] & Aj[x]);
                     cnt += c;
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 if (i >= d - 1) break;
                 const int wi = i >> 5;
                 const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
-                const unsigned ri = (unsigned)RW[i];
+                const unsigned ri = use_rw ? (unsigned)RW[i] : ((unsigned)wi << 16) | (unsigned)W;
                 for (int w = max(wi, (int)(ri >> 16)); w < (int)(ri & 0xffffu); ++w) {
                     unsigned bits = Ai[w];
                     while (bits) {

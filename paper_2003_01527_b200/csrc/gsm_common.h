@@ -215,7 +215,7 @@ struct Knobs {
     int clique_hub_ratio = 64;  // GSM_CLIQUE_HUB_RATIO: lookups when 32 nj <= ratio |N+(S[i])|
     int filter_u = 1;         // GSM_FILTER_U: K1 groups of 4 vertices per thread per pass (1, 2, 4; R-MAT-24: 0.063 / 0.086 / 0.126 ms)
     int clique_ranges = 1;    // GSM_CLIQUE_RANGES: K4 level 3 over the rows' nonzero word ranges
-    int bigsort = 1;          // GSM_BIGSORT (load): long lists by one radix sort instead of the segmented sort
+    int bigsort = 0;          // GSM_BIGSORT (load): long lists by one radix sort (R-MAT-24 relabel 52.9 vs 50.1 ms: off)
     int lidx_min = 32;        // GSM_LIDX_MIN (read at gsm_load_graph): label index for degree >= this (0 = none)
     int nhash_min = 16;       // GSM_NHASH_MIN (read at gsm_load_graph): hashed N+(v) for |N+(v)| >= this (0 = none)
     int clique_nh_stream = 64;  // GSM_CLIQUE_NH_STREAM: with a table, stream N+(S[i]) when 32 len <= this x nj

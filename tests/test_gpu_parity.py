@@ -726,10 +726,12 @@ def test_merge_rows():
         assert_rows_equal(out, oracle.sort_rows(np.concatenate([a, b]).reshape(-1, w)), f"merge w={w} {na}+{nb}")
 
 
-def test_long_lists_relabel():
-    """gsm_load_graph sorts the relabelled lists of degree >= 8192 by one radix sort of (list,
-    id) keys instead of the segmented sort: a hub of degree 12,000 plus a second one of 9,000
-    over random edges — K3 / P3 / C4 counts and K3 rows equal the oracle's."""
+@pytest.mark.parametrize("bigsort", ["0", "1"])
+def test_long_lists_relabel(bigsort, monkeypatch):
+    """gsm_load_graph's relabel with lists of degree >= 8192: by the segmented sort (default) or
+    by one radix sort of (list, id) keys (GSM_BIGSORT=1): a hub of degree 12,000 plus a second
+    one of 9,000 over random edges — K3 / P3 / C4 counts and K3 rows equal the oracle's."""
+    monkeypatch.setenv("GSM_BIGSORT", bigsort)
     rng = np.random.default_rng(21)
     n = 12500
     src = [np.zeros(12000, np.int64), np.ones(9000, np.int64)]

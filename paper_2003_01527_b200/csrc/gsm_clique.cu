@@ -92,25 +92,6 @@ __device__ __forceinline__ bool ck_has(const int32_t* Tk, unsigned P, unsigned s
     return (Tk[ck_h0(v, P, seed)] == v) | (Tk[P + ck_h1(v, P, seed)] == v);
 }
 
-// bit c of a hub bitmap row for the live lanes of a warp (columns c ascending over the lanes, as
-// S is sorted): when the live columns span at most 32 words, ONE coalesced 128-byte load of those
-// words plus a shuffle per lane replaces up to 32 scattered sector loads (R-MAT's hub neighbours
-// cluster at the top ranks); otherwise each live lane loads its own word.  hr[x] is valid for
-// x in [row/32, hw).  Must be called by the whole warp.
-__device__ __forceinline__ bool hub_bits_lookup(const uint32_t* __restrict__ hr, int hw, bool live, int c) {
-    const unsigned lm = __ballot_sync(kFull, live);
-    if (!lm) return false;
-    const int fl = __ffs(lm) - 1, ll = 31 - __clz(lm);
-    const int wlo = __shfl_sync(kFull, c, fl) >> 5, whi = __shfl_sync(kFull, c, ll) >> 5;
-    if (whi - wlo < 32) {
-        const int x = wlo + (threadIdx.x & 31);
-        const uint32_t wd = x < hw ? __ldg(hr + x) : 0u;
-        const uint32_t mine = __shfl_sync(kFull, wd, live ? (c >> 5) - wlo : 0);
-        return live && ((mine >> (c & 31)) & 1u);
-    }
-    return live && ((__ldg(hr + (c >> 5)) >> (c & 31)) & 1u);
-}
-
 }  // namespace
 
 struct BucketEdges {
@@ -217,7 +198,11 @@ __global__ void __launch_bounds__(256) k_clique_warp(CliqueArgs a) {
                 // hub pivot: S[j] > S[i] >= hub_base, one bitmap word per lane (L2-resident)
                 const uint32_t* hr = hub_row(a.hub_bits, a.hub_words, ai - a.hub_base);
                 const bool live = lane > i && lane < d;
-                const bool f = hub_bits_lookup(hr, a.hub_words, live, live ? sv - a.hub_base : 0);
+                bool f = false;
+                if (live) {
+                    const int c = sv - a.hub_base;
+                    f = (__ldg(hr + (c >> 5)) >> (c & 31)) & 1u;
+                }
                 bits = __ballot_sync(kFull, f);
                 items += live;
             } else if (ai_nh >= 0 && 32 * (le - ls) > (int64_t)a.nh_stream * nj) {
@@ -488,7 +473,11 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 for (int w = w0; w < W; ++w) {
                     const int j = (w << 5) + lane;
                     const bool live = j > i && j < d;
-                    const bool f = hub_bits_lookup(hr, a.hub_words, live, live ? S[j] - a.hub_base : 0);
+                    bool f = false;
+                    if (live) {
+                        const int c = S[j] - a.hub_base;
+                        f = (__ldg(hr + (c >> 5)) >> (c & 31)) & 1u;
+                    }
                     items += live;
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {

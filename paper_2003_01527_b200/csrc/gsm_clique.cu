@@ -292,7 +292,7 @@ struct CtaLay {
     int64_t smem_ints, slab_ints;
 };
 
-__host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool hash) {
+__host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool hash, bool ranges) {
     CtaLay L;
     int64_t o = 0, g = 0;
     const int W = (dmax + 31) >> 5;
@@ -309,7 +309,7 @@ __host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool has
     L.rh = q;
     q += dmax;
     L.rw = q;  // K4: nonzero word range of each bit row, lo << 16 | hi (hi exclusive)
-    q += K == 4 ? dmax : 0;
+    q += (K == 4 && ranges) ? dmax : 0;  // only with GSM_CLIQUE_RANGES (keeps the 960-root CTAs 2 per SM)
     q = (q + 1) & ~1LL;  // int64 alignment
     L.rb = q;
     q += 2 * (int64_t)dmax;
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     __shared__ unsigned long long sRoot;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int32_t* __restrict__ cols = a.cols;
-    const CtaLay L = cta_lay(K, a.dmax, kGlobal, a.use_hash != 0);
+    const CtaLay L = cta_lay(K, a.dmax, kGlobal, a.use_hash != 0, a.ranges != 0);
     int32_t* ws = kGlobal ? a.slab + (int64_t)blockIdx.x * L.slab_ints : csm;
     int32_t* Tk = csm + L.h;  // cuckoo keys [2P], then local indices [2P] (Tj)
     __shared__ int sFail;
@@ -688,7 +688,7 @@ static int sm_count() {
 static int use_hash() { return knobs().clique_hash ? 1 : 0; }  // 0: every row by binary search (tests)
 
 static size_t cta_smem(int K, int dmax, bool global) {
-    return sizeof(int32_t) * (size_t)cta_lay(K, dmax, global, use_hash() != 0).smem_ints;
+    return sizeof(int32_t) * (size_t)cta_lay(K, dmax, global, use_hash() != 0, knobs().clique_ranges != 0).smem_ints;
 }
 
 constexpr size_t kSmemLim = 216 * 1024;  // dynamic; + static (8 KB queues, counters) <= 227 KB
@@ -740,7 +740,7 @@ __global__ void k_gather_roots(const int32_t* __restrict__ roots, const int32_t*
 static int clique_dglob(int K) {
     int d = 1024;
     while (cta_smem(K, d + 256, true) <= kSmemLim &&
-           (double)cta_lay(K, d + 256, true, true).slab_ints * 4.0 * 148 <= 4e9)
+           (double)cta_lay(K, d + 256, true, true, true).slab_ints * 4.0 * 148 <= 4e9)
         d += 256;
     if (knobs().clique_dmax > 0) d = std::min(d, std::max(8, knobs().clique_dmax));
     return d;
@@ -847,7 +847,7 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
             GSM_LAUNCH("k_clique_warp");
         } else if (b == kNB - 2) {
             const int64_t blocks = std::min<int64_t>(nb, sms);
-            const CtaLay L = cta_lay(K, a.dmax, true, a.use_hash != 0);
+            const CtaLay L = cta_lay(K, a.dmax, true, a.use_hash != 0, a.ranges != 0);
             slab.ensure((size_t)blocks * L.slab_ints, s);
             a.slab = slab.p;
             a.slab_blocks = (int32_t)blocks;

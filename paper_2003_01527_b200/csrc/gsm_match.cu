@@ -417,11 +417,13 @@ void Matcher::run() {
         }
         res_->prof[GSM_K_EXPAND].alg_bytes += eb;
         if (clique_) {
-            // per root: id + offset pair + up (28 B); per S(u) entry: the entry and its own
-            // offset pair + up (4 + 20 B); list entries streamed and binary-search probes (4 B)
+            // per root: id + packed N+ descriptor (4 + 16 B); per S(u) entry: the entry and its
+            // descriptor (4 + 16 B); row items — list entries streamed, hub-bitmap words, keys
+            // looked up — 4 B each; a hashed-N+ bucket probe (or binary-search probe) 32 B (the
+            // bucket is one sector and the test must read all of it)
             const unsigned long long* st = hs.data();
             res_->prof[GSM_K_CLIQUE].alg_bytes +=
-                28.0 * (double)R0 + 24.0 * (double)st[4] + 4.0 * (double)st[0] + 4.0 * (double)st[1];
+                20.0 * (double)R0 + 20.0 * (double)st[4] + 4.0 * (double)st[0] + 32.0 * (double)st[1];
             res_->level_work[k_ - 1] += st[0];
         }
         if (pair_) {  // staged row + both plans' segments; candidates and probes

@@ -40,7 +40,7 @@ def parse_args():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--workload", default=os.environ.get("GSM_BENCH_WORKLOAD", "rmat24"))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--e2e-steps", type=int, default=1)
+    p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="oracle sample budget per pass (cpu_baseline)")
     p.add_argument("--refine-rounds", type=int, default=0, help="NE filter rounds (Alg. 1 lines 7-8)")

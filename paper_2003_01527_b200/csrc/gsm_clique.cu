@@ -719,14 +719,17 @@ static void launch_cta_mb(CliqueArgs a, int64_t blocks, cudaStream_t s) {
 
 // Round 1: registers capped for 2048 resident threads per SM (measured on R-MAT-24 K3+K4 then:
 // capped 760 ms vs uncapped 1,110 ms per step — the rows were latency-bound).
-// Round 2 (hub-bitmap / hashed rows, fewer registers of state): uncapped is faster — interleaved
-// A/B on R-MAT-24 K3+K4 377 ms capped (spills 20-40 B) vs 350 ms uncapped.  GSM_CLIQUE_OCC:
-// 0 = uncapped (default), 1 = cap for 2,048 resident threads, 2 = cap for 1,536.
+// Round 2 (hub-bitmap / hashed rows): interleaved A/B on R-MAT-24 K3+K4 — cap for 2,048
+// resident threads 378 ms (spills 20-40 B), uncapped 350 ms, cap for 1,536 threads 337 ms.
+// GSM_CLIQUE_OCC: 0 = uncapped, 1 = cap for 2,048, 2 = cap for 1,536 (default), 3 = for 1,280.
 template <int K, bool G, int NT>
 static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
-    if (knobs().clique_occ == 1) launch_cta_mb<K, G, NT, 2048 / NT>(a, blocks, s);
-    else if (knobs().clique_occ == 2) launch_cta_mb<K, G, NT, (1536 / NT > 0 ? 1536 / NT : 1)>(a, blocks, s);
-    else launch_cta_mb<K, G, NT, 1>(a, blocks, s);
+    switch (knobs().clique_occ) {
+        case 1: launch_cta_mb<K, G, NT, 2048 / NT>(a, blocks, s); break;
+        case 2: launch_cta_mb<K, G, NT, (1536 / NT > 0 ? 1536 / NT : 1)>(a, blocks, s); break;
+        case 3: launch_cta_mb<K, G, NT, (1280 / NT > 0 ? 1280 / NT : 1)>(a, blocks, s); break;
+        default: launch_cta_mb<K, G, NT, 1>(a, blocks, s); break;
+    }
 }
 
 // bucket edges on |S(u)|: warp kernel up to kEdge[0]; CTA kernels up to each next edge

@@ -719,6 +719,14 @@ static void launch_cta_mb(CliqueArgs a, int64_t blocks, cudaStream_t s) {
 
 // Round 1: registers capped for 2048 resident threads per SM (measured on R-MAT-24 K3+K4 then:
 // capped 760 ms vs uncapped 1,110 ms per step — the rows were latency-bound).
+template <int K, bool G, int NT, int MB>
+static int cta_occupancy_mb(size_t smem) {
+    GSM_CUDA(cudaFuncSetAttribute(k_clique_cta<K, G, NT, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLim));
+    int per_sm = 0;
+    GSM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_clique_cta<K, G, NT, MB>, NT, smem));
+    return per_sm;
+}
+
 // Round 2 (hub-bitmap / hashed rows): interleaved A/B on R-MAT-24 K3+K4 — cap for 2,048
 // resident threads 378 ms (spills 20-40 B), uncapped 350 ms, cap for 1,536 threads 337 ms.
 // GSM_CLIQUE_OCC: 0 = uncapped, 1 = cap for 2,048, 2 = cap for 1,536 (default), 3 = for 1,280.
@@ -729,6 +737,16 @@ static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
         case 2: launch_cta_mb<K, G, NT, (1536 / NT > 0 ? 1536 / NT : 1)>(a, blocks, s); break;
         case 3: launch_cta_mb<K, G, NT, (1280 / NT > 0 ? 1280 / NT : 1)>(a, blocks, s); break;
         default: launch_cta_mb<K, G, NT, 1>(a, blocks, s); break;
+    }
+}
+
+template <int K, bool G, int NT>
+static int cta_occupancy(size_t smem) {
+    switch (knobs().clique_occ) {
+        case 1: return cta_occupancy_mb<K, G, NT, 2048 / NT>(smem);
+        case 2: return cta_occupancy_mb<K, G, NT, (1536 / NT > 0 ? 1536 / NT : 1)>(smem);
+        case 3: return cta_occupancy_mb<K, G, NT, (1280 / NT > 0 ? 1280 / NT : 1)>(smem);
+        default: return cta_occupancy_mb<K, G, NT, 1>(smem);
     }
 }
 
@@ -860,13 +878,16 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
             a.slab_blocks = (int32_t)blocks;
             launch_cta<K, true, 1024>(a, blocks, s);
         } else {
-            // CTA size with the most resident warps per SM for this bucket's shared memory
-            // (ties -> smaller CTAs: finer-grained root scheduling)
+            // CTA size with the most resident warps per SM for this bucket's shared memory and
+            // the instantiation's registers (the runtime's occupancy calculator; ties -> smaller
+            // CTAs: finer-grained root scheduling)
             const size_t sm = cta_smem(K, a.dmax, false);
             int best = 256, bestw = -1;
             for (int nt : {256, 512, 1024}) {
                 const size_t per = sm + sizeof(int32_t) * 64 * (nt / 32) + 64 + 1024;  // + static + reserved
-                const int ctas = std::min<int>(2048 / nt, (int)((228 * 1024) / per));
+                const int ctas = !knobs().clique_ntsel ? std::min<int>(2048 / nt, (int)((228 * 1024) / per))
+                               : nt == 256 ? cta_occupancy<K, false, 256>(sm)
+                               : nt == 512 ? cta_occupancy<K, false, 512>(sm) : cta_occupancy<K, false, 1024>(sm);
                 if (ctas * nt / 32 > bestw) {
                     bestw = ctas * nt / 32;
                     best = nt;

@@ -736,6 +736,7 @@ static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
         case 1: launch_cta_mb<K, G, NT, 2048 / NT>(a, blocks, s); break;
         case 2: launch_cta_mb<K, G, NT, (1536 / NT > 0 ? 1536 / NT : 1)>(a, blocks, s); break;
         case 3: launch_cta_mb<K, G, NT, (1280 / NT > 0 ? 1280 / NT : 1)>(a, blocks, s); break;
+        case 4: launch_cta_mb<K, G, NT, (1024 / NT > 0 ? 1024 / NT : 1)>(a, blocks, s); break;
         default: launch_cta_mb<K, G, NT, 1>(a, blocks, s); break;
     }
 }
@@ -746,6 +747,7 @@ static int cta_occupancy(size_t smem) {
         case 1: return cta_occupancy_mb<K, G, NT, 2048 / NT>(smem);
         case 2: return cta_occupancy_mb<K, G, NT, (1536 / NT > 0 ? 1536 / NT : 1)>(smem);
         case 3: return cta_occupancy_mb<K, G, NT, (1280 / NT > 0 ? 1280 / NT : 1)>(smem);
+        case 4: return cta_occupancy_mb<K, G, NT, (1024 / NT > 0 ? 1024 / NT : 1)>(smem);
         default: return cta_occupancy_mb<K, G, NT, 1>(smem);
     }
 }

@@ -727,9 +727,10 @@ static int cta_occupancy_mb(size_t smem) {
     return per_sm;
 }
 
-// Round 2 (hub-bitmap / hashed rows): interleaved A/B on R-MAT-24 K3+K4 — cap for 2,048
-// resident threads 378 ms (spills 20-40 B), uncapped 350 ms, cap for 1,536 threads 337 ms.
-// GSM_CLIQUE_OCC: 0 = uncapped, 1 = cap for 2,048, 2 = cap for 1,536 (default), 3 = for 1,280.
+// Round 2 (hub-bitmap / hashed rows): interleaved A/B on R-MAT-24 K3+K4 (profiles/r2_ab*.jsonl)
+// — cap for 2,048 resident threads 378 ms (spills 20-40 B), uncapped 350, 1,536 337, 1,280 333,
+// and 1,280 with the bucket CTA size from the occupancy calculator 323 ms (1,024: 346).
+// GSM_CLIQUE_OCC: 0 = uncapped, 1 = 2,048, 2 = 1,536, 3 = 1,280 (default), 4 = 1,024 threads.
 template <int K, bool G, int NT>
 static void launch_cta(CliqueArgs a, int64_t blocks, cudaStream_t s) {
     switch (knobs().clique_occ) {

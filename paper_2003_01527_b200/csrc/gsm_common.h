@@ -194,7 +194,7 @@ struct Knobs {
     int clique_dmax = 0;      // GSM_CLIQUE_DMAX: cap of the global-slab bucket (0 = max fitting)
     int clique_stream = 128;  // GSM_CLIQUE_STREAM: stream-vs-search threshold (x/32 per remaining entry)
     int clique_hash = 1;      // GSM_CLIQUE_HASH: 0 = rows by binary search only
-    int clique_occ = 2;       // GSM_CLIQUE_OCC: register cap for 0 uncapped / 1 2048 / 2 1536 / 3 1280 resident threads
+    int clique_occ = 3;       // GSM_CLIQUE_OCC: register cap for 0 uncapped / 1 2048 / 2 1536 / 3 1280 / 4 1024 resident threads
     int pair_tail = 1;        // GSM_PAIR_TAIL
     int pair_thread_max = 16; // GSM_PAIR_THREAD_MAX
     int fused_tail = 1;       // GSM_FUSED_TAIL

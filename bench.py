@@ -203,22 +203,53 @@ def oracle_pass(g, queries, roots):
     return uni, time.perf_counter() - t0
 
 
-def _pass_child(conn, g, queries, roots):
+_SHM = {}  # id(graph) -> directory of its .npy arrays for spawned oracle children
+
+
+def _graph_files(g):
+    """The graph's arrays as .npy files (in /dev/shm when present) for a spawned child to mmap."""
+    import tempfile
+
+    import numpy as np
+    key = id(g)
+    if key not in _SHM:
+        d = tempfile.mkdtemp(prefix="gsm_oracle_", dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+        np.save(os.path.join(d, "offsets.npy"), g.offsets)
+        np.save(os.path.join(d, "cols.npy"), g.cols)
+        if g.labels is not None:
+            np.save(os.path.join(d, "labels.npy"), g.labels)
+        import atexit
+        import shutil
+        atexit.register(shutil.rmtree, d, True)
+        _SHM[key] = d
+    return _SHM[key]
+
+
+def _pass_child(conn, d, n, queries, roots):
+    import numpy as np
+
+    import gsm_inputs as gi
+    lab = os.path.join(d, "labels.npy")
+    g = gi.Graph(n, np.load(os.path.join(d, "offsets.npy"), mmap_mode="r"),
+                 np.load(os.path.join(d, "cols.npy"), mmap_mode="r"),
+                 np.load(lab, mmap_mode="r") if os.path.exists(lab) else None)
     conn.send(oracle_pass(g, queries, roots))
     conn.close()
 
 
 def oracle_pass_bounded(g, queries, roots, limit_s: float):
-    """oracle_pass in a forked child (the graph is shared copy-on-write), killed after
-    limit_s: per-root DFS cost is heavy-tailed (one R-MAT hub root can take hours), so a
-    calibration pass must be interruptible without touching the oracle.  None on timeout."""
+    """oracle_pass in a SPAWNED child (the graph mmapped from .npy files), killed after limit_s:
+    per-root DFS cost is heavy-tailed (one R-MAT hub root can take hours), so a calibration pass
+    must be interruptible without touching the oracle.  Spawn, not fork: a forked child of a
+    process whose OpenMP runtime (input generator) or CUDA context is live hangs (measured: every
+    forked pass timed out and the sample shrank to one root).  None on timeout."""
     import multiprocessing as mp
-    ctx = mp.get_context("fork")
+    ctx = mp.get_context("spawn")
     a, b = ctx.Pipe(duplex=False)
-    p = ctx.Process(target=_pass_child, args=(b, g, queries, roots), daemon=True)
+    p = ctx.Process(target=_pass_child, args=(b, _graph_files(g), g.num_nodes, queries, roots), daemon=True)
     p.start()
     b.close()
-    res = a.recv() if a.poll(limit_s) else None
+    res = a.recv() if a.poll(limit_s + 10.0) else None  # + interpreter start-up
     if p.is_alive():
         p.kill()
     p.join()
@@ -256,7 +287,7 @@ def oracle_sample(g, queries, target_s: float):
 
 def cpu_baseline(g, w, budget_s):
     roots, uni, dt, threads = oracle_sample(g, w.queries, budget_s)
-    return {"value": uni / dt if dt > 0 else None, "unit": METRIC, "cores": threads, "kind": "oracle",
+    return {"value": uni / dt if (dt > 0 and uni > 0) else None, "unit": METRIC, "cores": threads, "kind": "oracle",
             "sample": f"all embeddings of {[q.name for q in w.queries]} with f(query vertex 0) in a fixed evenly "
                       f"strided sample of {len(roots)} of {g.num_nodes} vertices, counted as all/|Aut(Q)|; "
                       f"{uni:.6g} unique-equivalent embeddings in {dt:.2f} s (one pass)"}
@@ -325,8 +356,6 @@ def run_ours(args, world, rank, local, dist):
     from gsm_inputs import workloads
     from paper_2003_01527_b200 import gsm
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     if not args.clique:
         os.environ["GSM_CLIQUE"] = "0"  # read by the library at every gsm_match
     w = workloads.get(args.workload)
@@ -338,6 +367,17 @@ def run_ours(args, world, rank, local, dist):
             g = w.graph()
     else:
         g = w.graph()
+    # the oracle baseline runs BEFORE this process touches CUDA: its calibration forks children
+    # (killable when a strided sample hits a hub root), and forking a process with a live CUDA
+    # context is unsafe (measured: every child died, the sample shrank to one root)
+    cpu_base = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu_base = cpu_baseline(g, w, args.cpu_seconds)
+        except Exception as e:  # baseline failure must not hide the measurement
+            cpu_base = {"value": None, "error": repr(e)}
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=local)
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
@@ -513,11 +553,8 @@ def run_ours(args, world, rank, local, dist):
            "counts_per_step": {"all": c_all, "unique": c_uni},
            "all_per_s": c_all / (ms / 1000.0),
            "query_ms": ms, "per_query_rank0": per_query, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            out["cpu_baseline"] = cpu_baseline(g, w, args.cpu_seconds)
-        except Exception as e:  # baseline failure must not hide the measurement
-            out["cpu_baseline"] = {"value": None, "error": repr(e)}
+    if cpu_base is not None:
+        out["cpu_baseline"] = cpu_base
     print(json.dumps(out), flush=True)
 
 

@@ -51,7 +51,11 @@ def time_match(G, q, reps, root_subset=None):
     return cnt, statistics.mean(ts), statistics.median(ts)
 
 
-def _child(conn, g, q, roots):
+def _child(conn, d, n, q, roots):
+    lab = os.path.join(d, "labels.npy")
+    g = gi.Graph(n, np.load(os.path.join(d, "offsets.npy"), mmap_mode="r"),
+                 np.load(os.path.join(d, "cols.npy"), mmap_mode="r"),
+                 np.load(lab, mmap_mode="r") if os.path.exists(lab) else None)
     t0 = time.perf_counter()
     c = oracle.match(g, q, roots=roots, count_only=True)[0]
     conn.send((c, time.perf_counter() - t0))
@@ -59,12 +63,15 @@ def _child(conn, g, q, roots):
 
 
 def oracle_bounded(g, q, roots, limit_s):
-    ctx = mp.get_context("fork")
+    """The oracle's count in a SPAWNED child (graph mmapped from .npy files; a forked child of
+    this CUDA process hangs), killed after limit_s.  None on timeout."""
+    import bench
+    ctx = mp.get_context("spawn")
     a, b = ctx.Pipe(duplex=False)
-    p = ctx.Process(target=_child, args=(b, g, q, roots), daemon=True)
+    p = ctx.Process(target=_child, args=(b, bench._graph_files(g), g.num_nodes, q, roots), daemon=True)
     p.start()
     b.close()
-    res = a.recv() if a.poll(limit_s) else None
+    res = a.recv() if a.poll(limit_s + 10.0) else None
     if p.is_alive():
         p.kill()
     p.join()

@@ -82,6 +82,7 @@ void load_knobs() {
     k.lidx_min = std::max(0, env_or("GSM_LIDX_MIN", k.lidx_min));
     k.clique_ranges = env_or("GSM_CLIQUE_RANGES", k.clique_ranges);
     k.clique_ntsel = env_or("GSM_CLIQUE_NTSEL", k.clique_ntsel);
+    k.clique_ne = env_or("GSM_CLIQUE_NE", k.clique_ne);
     k.bigsort = env_or("GSM_BIGSORT", k.bigsort);
     {
         const int fu = env_or("GSM_FILTER_U", k.filter_u);

@@ -367,15 +367,6 @@ def run_ours(args, world, rank, local, dist):
             g = w.graph()
     else:
         g = w.graph()
-    # the oracle baseline runs BEFORE this process touches CUDA: its calibration forks children
-    # (killable when a strided sample hits a hub root), and forking a process with a live CUDA
-    # context is unsafe (measured: every child died, the sample shrank to one root)
-    cpu_base = None
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu_base = cpu_baseline(g, w, args.cpu_seconds)
-        except Exception as e:  # baseline failure must not hide the measurement
-            cpu_base = {"value": None, "error": repr(e)}
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=local)
@@ -553,8 +544,14 @@ def run_ours(args, world, rank, local, dist):
            "counts_per_step": {"all": c_all, "unique": c_uni},
            "all_per_s": c_all / (ms / 1000.0),
            "query_ms": ms, "per_query_rank0": per_query, "roofline": roof, "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e}
-    if cpu_base is not None:
-        out["cpu_baseline"] = cpu_base
+    # the oracle baseline runs AFTER the timed GPU work (its 16-thread passes must not share the
+    # host with the timed steps), in spawned children (oracle_pass_bounded): spawn is safe from a
+    # process with a live CUDA context, fork was not
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(g, w, args.cpu_seconds)
+        except Exception as e:  # baseline failure must not hide the measurement
+            out["cpu_baseline"] = {"value": None, "error": repr(e)}
     print(json.dumps(out), flush=True)
 
 

@@ -48,6 +48,8 @@ def time_match(G, q, reps, root_subset=None):
         r.free()
         if i:
             ts.append(a.elapsed_time(b))
+    if not ts:  # reps == 0: the one (warm-up) run is the only sample
+        return cnt, None, None
     return cnt, statistics.mean(ts), statistics.median(ts)
 
 

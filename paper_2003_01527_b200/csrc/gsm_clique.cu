@@ -151,6 +151,7 @@ struct CliqueArgs {
     int32_t nh_stream;      // with a table, a row streams N+(S[i]) only when 32 |N+(S[i])| <= nh_stream x nj
     int32_t ranges;         // K4: level 3 over the overlap of the rows' nonzero word ranges (else j/32..W)
     int32_t ne_mask;        // K4: level 3 skips pairs (i, j) whose row A[j] is empty
+    int32_t lazy_ck;        // build the per-root cuckoo table only when some row streams
     int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
     int32_t slab_blocks;    // kGlobal: slabs allocated (the grid must not exceed it)
     unsigned long long* next;   // dynamic root scheduler
@@ -392,6 +393,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
         }
         // S(u) and, per entry, its own list N+(S[j]) (one parallel gather instead of a
         // dependent chain per row)
+        int wants_stream = 0;  // some row of this root would stream N+(S[i]) (needs the cuckoo table)
         for (int j = threadIdx.x; j < d; j += NT) {
             const int32_t v = cols[s0 + j];
             S[j] = v;
@@ -402,14 +404,19 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             RB[j] = b;
             RL[j] = len;
             RH[j] = nh;
+            // the row loop's choice, given a table: hub lookups / hashed lookups / stream
+            const int64_t nj = d - 1 - j;
+            const bool hub = a.hub_bits && v >= a.hub_base && 32 * nj <= (int64_t)a.hub_ratio * len;
+            const int64_t thr = nh >= 0 ? a.nh_stream : a.stream_max;
+            wants_stream |= (nj > 0 && !hub && 32LL * len <= thr * nj) ? 1 : 0;
         }
         if (threadIdx.x == 0) sent += d;
         if (K == 4)
             for (int w = threadIdx.x; w < W; w += NT) NE[w] = 0u;
-        // cuckoo build (a failed build — an eviction cycle — retries with a new seed; after
-        // 4 failures the root's rows all take the binary-search strategy)
+        // cuckoo build, only if some row streams (a failed build — an eviction cycle — retries
+        // with a new seed; after 4 failures the root's rows all take the binary-search strategy)
         unsigned seed = 0;
-        bool use_ck = a.use_hash != 0;
+        bool use_ck = __syncthreads_or(wants_stream | !a.lazy_ck) && a.use_hash != 0;
         for (; use_ck; ++seed) {
             if (seed == 4) {
                 use_ck = false;
@@ -854,6 +861,7 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     a.nh_stream = knobs().clique_nh_stream;
     a.ranges = knobs().clique_ranges;
     a.ne_mask = knobs().clique_ne;
+    a.lazy_ck = knobs().clique_lazy_ck;
     DevBuf<unsigned long long> cyc;
     a.cyc = nullptr;
     if (knobs().trace == 2) {

@@ -150,7 +150,6 @@ struct CliqueArgs {
     const int32_t* nh_tab;
     int32_t nh_stream;      // with a table, a row streams N+(S[i]) only when 32 |N+(S[i])| <= nh_stream x nj
     int32_t ranges;         // K4: level 3 over the overlap of the rows' nonzero word ranges (else j/32..W)
-    int32_t ne_mask;        // K4: level 3 skips pairs (i, j) whose row A[j] is empty
     int32_t lazy_ck;        // build the per-root cuckoo table only when some row streams
     int32_t* slab;          // kGlobal: per-CTA scratch of cta_lay(..).slab_ints ints
     int32_t slab_blocks;    // kGlobal: slabs allocated (the grid must not exceed it)
@@ -290,7 +289,7 @@ __host__ __device__ inline int64_t tri_words(int d) {
 }
 
 struct CtaLay {
-    int64_t h, tb, s, rl, rh, rw, ne, rb, A;  // offsets (int32 units) in shared memory or the slab
+    int64_t h, tb, s, rl, rh, rw, rb, A;  // offsets (int32 units) in shared memory or the slab
     int64_t smem_ints, slab_ints;
 };
 
@@ -312,8 +311,6 @@ __host__ __device__ inline CtaLay cta_lay(int K, int dmax, bool global, bool has
     q += dmax;
     L.rw = q;  // K4: nonzero word range of each bit row, lo << 16 | hi (hi exclusive)
     q += (K == 4 && ranges) ? dmax : 0;  // only with GSM_CLIQUE_RANGES (keeps the 960-root CTAs 2 per SM)
-    L.ne = q;  // K4: bit i set iff bit row A[i] is not all zero (level 3 skips pairs with an empty A[j])
-    q += K == 4 ? W : 0;
     q = (q + 1) & ~1LL;  // int64 alignment
     L.rb = q;
     q += 2 * (int64_t)dmax;
@@ -343,7 +340,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
     int32_t* RL = ws + L.rl;
     int32_t* RH = ws + L.rh;  // nh_off of each S entry (-1: no hashed N+)
     int32_t* RW = ws + L.rw;  // K4: nonzero word range [lo, hi) of bit row i, lo << 16 | hi
-    unsigned* NE = reinterpret_cast<unsigned*>(ws + L.ne);  // K4: nonempty-row mask
     int64_t* RB = reinterpret_cast<int64_t*>(ws + L.rb);
     unsigned* A = reinterpret_cast<unsigned*>(ws + L.A);
     unsigned long long cnt = 0;
@@ -411,8 +407,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             wants_stream |= (nj > 0 && !hub && 32LL * len <= thr * nj) ? 1 : 0;
         }
         if (threadIdx.x == 0) sent += d;
-        if (K == 4)
-            for (int w = threadIdx.x; w < W; w += NT) NE[w] = 0u;
         // cuckoo build, only if some row streams (a failed build — an eviction cycle — retries
         // with a new seed; after 4 failures the root's rows all take the binary-search strategy)
         unsigned seed = 0;
@@ -479,7 +473,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
             const int64_t le = ls + len;
             const int nj = d - 1 - i;
             const int32_t ai = S[i];
-            unsigned rowany = 0;  // K4: OR of the row's words (nonempty-row mask NE)
             if (a.hub_bits && ai >= a.hub_base && 32LL * nj <= (int64_t)a.hub_ratio * len) {
                 // hub pivot: every S[j] (j > i) is a hub too; bit j of A[i] = one word of the
                 // L2-resident hub bitmap row of S[i] (replaces the stream / binary search)
@@ -496,12 +489,10 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
                         if (lane == 0) Ai[w] = bits;
-                        rowany |= bits;
                     } else {
                         cnt += f;
                     }
                 }
-                if (K == 4 && lane == 0 && rowany) atomicOr(&NE[i >> 5], 1u << (i & 31));
                 if (a.cyc) {
                     const long long t1 = clock64();
                     trace(2, t1 - tc, nj, 4);
@@ -522,12 +513,10 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
                         if (lane == 0) Ai[w] = bits;
-                        rowany |= bits;
                     } else {
                         cnt += f;
                     }
                 }
-                if (K == 4 && lane == 0 && rowany) atomicOr(&NE[i >> 5], 1u << (i & 31));
                 if (a.cyc) {
                     const long long t1 = clock64();
                     trace(2, t1 - tc, nj, 5);
@@ -553,7 +542,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     if (K == 4) {
                         if (j0 >= 0) atomicOr(&Ai[j0 >> 5], 1u << (j0 & 31));
                         if (j1 >= 0) atomicOr(&Ai[j1 >> 5], 1u << (j1 & 31));
-                        rowany |= __ballot_sync(kFull, (j0 >= 0) | (j1 >= 0));
                     } else {
                         cnt += (j0 >= 0) + (j1 >= 0);
                     }
@@ -587,7 +575,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     const unsigned bits = __ballot_sync(kFull, f);
                     if (K == 4) {
                         if (lane == 0) Ai[w] = bits;
-                        rowany |= bits;
                     } else {
                         cnt += f;
                     }
@@ -598,7 +585,6 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                     tc = t1;
                 }
             }
-            if (K == 4 && lane == 0 && rowany) atomicOr(&NE[i >> 5], 1u << (i & 31));
         }
         if (K == 3) continue;
         __syncthreads();
@@ -656,7 +642,7 @@ __global__ void __launch_bounds__(NT, kMinB) k_clique_cta(CliqueArgs a) {
                 const unsigned* Ai = A + TB[wi] + (i & 31) * TB[W + 1 + wi] - wi;
                 const unsigned ri = use_rw ? (unsigned)RW[i] : ((unsigned)wi << 16) | (unsigned)W;
                 for (int w = max(wi, (int)(ri >> 16)); w < (int)(ri & 0xffffu); ++w) {
-                    unsigned bits = Ai[w] & (a.ne_mask ? NE[w] : ~0u);
+                    unsigned bits = Ai[w];
                     while (bits) {
                         const int take = min(__popc(bits), 32 - nJ);
                         const bool has = (bits >> lane) & 1u;
@@ -860,7 +846,6 @@ static int64_t run_clique_k(CliqueRun& r, cudaStream_t s) {
     a.nh_tab = r.nh_tab;
     a.nh_stream = knobs().clique_nh_stream;
     a.ranges = knobs().clique_ranges;
-    a.ne_mask = knobs().clique_ne;
     a.lazy_ck = knobs().clique_lazy_ck;
     DevBuf<unsigned long long> cyc;
     a.cyc = nullptr;

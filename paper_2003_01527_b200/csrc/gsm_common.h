@@ -216,7 +216,6 @@ struct Knobs {
     int filter_u = 1;         // GSM_FILTER_U: K1 groups of 4 vertices per thread per pass (1, 2, 4; R-MAT-24: 0.063 / 0.086 / 0.126 ms)
     int clique_ntsel = 1;     // GSM_CLIQUE_NTSEL: CTA size per bucket from the occupancy calculator (0: shared memory only)
     int clique_lazy_ck = 1;   // GSM_CLIQUE_LAZYCK: per-root cuckoo table only when some row streams
-    int clique_ne = 1;        // GSM_CLIQUE_NE: K4 level 3 skips pairs whose second row is empty
     int clique_ranges = 0;    // GSM_CLIQUE_RANGES: K4 level 3 over the rows' nonzero word ranges (interleaved A/B on R-MAT-24: K4 269.5 on vs 260.4 ms off)
     int bigsort = 0;          // GSM_BIGSORT (load): long lists by one radix sort (R-MAT-24 relabel 52.9 vs 50.1 ms: off)
     int lidx_min = 32;        // GSM_LIDX_MIN (read at gsm_load_graph): label index for degree >= this (0 = none)

@@ -82,7 +82,6 @@ void load_knobs() {
     k.lidx_min = std::max(0, env_or("GSM_LIDX_MIN", k.lidx_min));
     k.clique_ranges = env_or("GSM_CLIQUE_RANGES", k.clique_ranges);
     k.clique_ntsel = env_or("GSM_CLIQUE_NTSEL", k.clique_ntsel);
-    k.clique_ne = env_or("GSM_CLIQUE_NE", k.clique_ne);
     k.clique_lazy_ck = env_or("GSM_CLIQUE_LAZYCK", k.clique_lazy_ck);
     k.bigsort = env_or("GSM_BIGSORT", k.bigsort);
     {

@@ -153,7 +153,7 @@ def dense_gnp():
 
 @pytest.mark.parametrize("variant", ["default", "nohub", "hubmix", "hubmix_warp0", "warp0", "dsmem64", "search",
                                      "stream", "nohash", "handback", "off", "nh_all", "nh_all_warp0", "nh_dsmem64",
-                                     "ranges", "ranges_dsmem64", "occ1", "occ0", "ne0", "eagerck"])
+                                     "ranges", "ranges_dsmem64", "occ1", "occ0", "eagerck"])
 def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
     """K3/K4 COUNT through the per-root local-bitmap kernels (gsm_clique.cu) in every
     bucket (warp per root; CTA with shared memory; CTA with a global slab via a tiny
@@ -179,7 +179,7 @@ def test_clique_bitmap_path(variant, dense_gnp, monkeypatch):
            "nh_dsmem64": {"GSM_NHASH_MIN": "1", "GSM_CLIQUE_NH_STREAM": "0", "GSM_CLIQUE_DSMEM": "64"},
            "ranges": {"GSM_CLIQUE_RANGES": "1"},
            "ranges_dsmem64": {"GSM_CLIQUE_RANGES": "1", "GSM_CLIQUE_DSMEM": "64"},
-           "occ1": {"GSM_CLIQUE_OCC": "1"}, "occ0": {"GSM_CLIQUE_OCC": "0"}, "ne0": {"GSM_CLIQUE_NE": "0"}, "eagerck": {"GSM_CLIQUE_LAZYCK": "0"}}.get(variant, {})
+           "occ1": {"GSM_CLIQUE_OCC": "1"}, "occ0": {"GSM_CLIQUE_OCC": "0"}, "eagerck": {"GSM_CLIQUE_LAZYCK": "0"}}.get(variant, {})
     if variant not in ("default", "hubmix", "hubmix_warp0"):
         env = {"GSM_HUB_BITS": "0", **env}
     if variant not in ("default", "hubmix", "hubmix_warp0") and not variant.startswith("nh_"):

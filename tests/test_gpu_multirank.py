@@ -1,6 +1,6 @@
 """Multi-rank path on one GPU (functional): two processes share cuda:0 and
 talk over gloo.  multigpu.match_sharded must reproduce the single-process
-result (count and the full sorted row list, merged with gsm_sort_rows), and
+result (count and the full sorted row list, merged by the gsm_merge_rows tree), and
 bench.py under torchrun must report the same total as one rank."""
 import json
 import os

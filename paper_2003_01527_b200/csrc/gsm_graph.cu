@@ -83,6 +83,7 @@ void load_knobs() {
     k.clique_ranges = env_or("GSM_CLIQUE_RANGES", k.clique_ranges);
     k.clique_ntsel = env_or("GSM_CLIQUE_NTSEL", k.clique_ntsel);
     k.clique_lazy_ck = env_or("GSM_CLIQUE_LAZYCK", k.clique_lazy_ck);
+    k.filter_bps = std::max(1, std::min(512, env_or("GSM_FILTER_BPS", k.filter_bps)));
     k.bigsort = env_or("GSM_BIGSORT", k.bigsort);
     {
         const int fu = env_or("GSM_FILTER_U", k.filter_u);

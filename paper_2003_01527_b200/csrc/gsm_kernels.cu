@@ -134,7 +134,7 @@ void launch_filter(const DevGraph& g, const FilterQuery& q, void* cmask, unsigne
                    cudaStream_t s) {
     // kU groups of 4 vertices per thread per pass (GSM_FILTER_U = 1, 2, 4); grid = SMs x resident blocks
     const int U = knobs().filter_u;
-    const int grid = grid_for((g.n + 4 * U - 1) / (4 * U), kThreads, 148 * 8 / U);
+    const int grid = grid_for((g.n + 4 * U - 1) / (4 * U), kThreads, 148 * knobs().filter_bps / U);
     auto go = [&](auto kern, auto* mask) { kern<<<grid, kThreads, 0, s>>>(g.off, g.labels, g.n, q, mask, counts); };
     const int mb = mask_bytes_for(q.k);
     if (U == 4) {

@@ -17,3 +17,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 1200 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/r2_final3_traffic_rmat24.csv $B > gpurun_out/ncu_ft3.log 2>&1
 timeout 600 python tools/load_phases.py rmat24 > gpurun_out/load_final3.log 2>&1; grep "load 2\|hashed\|relabelled\|upload" gpurun_out/load_final3.log | tail -4
 echo final3-done
+timeout 2400 python tools/sweep_fig3.py --axis labels --reps 10 --oracle-s 10 --queries 4 --out gpurun_out/r2_fig3_labels.jsonl > gpurun_out/r2_fig3_labels.log 2>&1
+echo rc=$? >> gpurun_out/r2_fig3_labels.log; tail -3 gpurun_out/r2_fig3_labels.log
+echo labels-done

@@ -130,6 +130,7 @@ def main():
     p.add_argument("--sample-roots", type=int, default=32)
     p.add_argument("--queries", type=int, default=10, help="random-walk queries per label count (P:220)")
     p.add_argument("--out", default="gpurun_out/fig3_sweep.jsonl")
+    p.add_argument("--axis", default="both", choices=["both", "sizes", "labels"])
     a = p.parse_args()
     ok = True
     with open(a.out, "w") as out:
@@ -138,7 +139,7 @@ def main():
         base = gi.rmat(15, 8, 1)
         g = base.with_labels(gi.zipf_labels(base.num_nodes, 20, 1), tag="-Z20")
         G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=0)
-        for k in range(3, 14):
+        for k in (range(3, 14) if a.axis in ("both", "sizes") else []):
             q = None
             for e in range(2 * k - 3, k - 2, -1):  # as dense as the walks allow
                 try:
@@ -150,7 +151,7 @@ def main():
         G.free()
         # (b) label count 20..200: 10 random-walk queries of 12 nodes / 22 edges each
         base = gi.rmat(17, 8, 1)
-        for L in (20, 50, 100, 150, 200):
+        for L in ((20, 50, 100, 150, 200) if a.axis in ("both", "labels") else ()):
             g = base.with_labels(gi.zipf_labels(base.num_nodes, L, 1), tag=f"-Z{L}")
             G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=0)
             made = 0

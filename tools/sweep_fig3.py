@@ -131,6 +131,7 @@ def main():
     p.add_argument("--queries", type=int, default=10, help="random-walk queries per label count (P:220)")
     p.add_argument("--out", default="gpurun_out/fig3_sweep.jsonl")
     p.add_argument("--axis", default="both", choices=["both", "sizes", "labels"])
+    p.add_argument("--label-scale", type=int, default=17, help="R-MAT scale of the label-axis graph")
     a = p.parse_args()
     ok = True
     with open(a.out, "w") as out:
@@ -150,7 +151,7 @@ def main():
             ok &= point(out, g, G, q, "query_size", k, a)
         G.free()
         # (b) label count 20..200: 10 random-walk queries of 12 nodes / 22 edges each
-        base = gi.rmat(17, 8, 1)
+        base = gi.rmat(a.label_scale, 8, 1)
         for L in ((20, 50, 100, 150, 200) if a.axis in ("both", "labels") else ()):
             g = base.with_labels(gi.zipf_labels(base.num_nodes, L, 1), tag=f"-Z{L}")
             G = gsm.gsm_load_graph(g.num_nodes, g.offsets, g.cols, g.labels, device=0)

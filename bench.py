@@ -203,7 +203,8 @@ def oracle_pass(g, queries, roots):
     return uni, time.perf_counter() - t0
 
 
-_SHM = {}  # id(graph) -> directory of its .npy arrays for spawned oracle children
+_SHM = {}  # id(graph) -> (graph, directory of its .npy arrays) for spawned oracle children;
+# the graph itself is kept referenced so its id cannot be reused by a later graph
 
 
 def _graph_files(g):
@@ -212,7 +213,7 @@ def _graph_files(g):
 
     import numpy as np
     key = id(g)
-    if key not in _SHM:
+    if key not in _SHM or _SHM[key][0] is not g:
         d = tempfile.mkdtemp(prefix="gsm_oracle_", dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
         np.save(os.path.join(d, "offsets.npy"), g.offsets)
         np.save(os.path.join(d, "cols.npy"), g.cols)
@@ -221,8 +222,8 @@ def _graph_files(g):
         import atexit
         import shutil
         atexit.register(shutil.rmtree, d, True)
-        _SHM[key] = d
-    return _SHM[key]
+        _SHM[key] = (g, d)
+    return _SHM[key][1]
 
 
 def _pass_child(conn, d, n, queries, roots):

@@ -217,6 +217,7 @@ struct Knobs {
     int clique_ntsel = 1;     // GSM_CLIQUE_NTSEL: CTA size per bucket from the occupancy calculator (0: shared memory only)
     int clique_lazy_ck = 1;   // GSM_CLIQUE_LAZYCK: per-root cuckoo table only when some row streams
     int clique_ranges = 0;    // GSM_CLIQUE_RANGES: K4 level 3 over the rows' nonzero word ranges (interleaved A/B on R-MAT-24: K4 269.5 on vs 260.4 ms off)
+    int bigsort_min = 8192;   // GSM_BIGSORT_MIN: list length from which GSM_BIGSORT takes a list
     int bigsort = 0;          // GSM_BIGSORT (load): long lists by one radix sort (R-MAT-24 relabel 52.9 vs 50.1 ms: off)
     int filter_bps = 8;       // GSM_FILTER_BPS: K1 grid = 148 x this blocks (grid-stride beyond)
     int lidx_min = 32;        // GSM_LIDX_MIN (read at gsm_load_graph): label index for degree >= this (0 = none)

@@ -85,6 +85,7 @@ void load_knobs() {
     k.clique_lazy_ck = env_or("GSM_CLIQUE_LAZYCK", k.clique_lazy_ck);
     k.filter_bps = std::max(1, std::min(512, env_or("GSM_FILTER_BPS", k.filter_bps)));
     k.bigsort = env_or("GSM_BIGSORT", k.bigsort);
+    k.bigsort_min = std::max(2, env_or("GSM_BIGSORT_MIN", k.bigsort_min));
     {
         const int fu = env_or("GSM_FILTER_U", k.filter_u);
         k.filter_u = (fu == 1 || fu == 2 || fu == 4) ? fu : 1;
@@ -684,7 +685,7 @@ static void load_graph_impl(int64_t n, const int64_t* row_offsets, const int32_t
         // R-MAT-24), so the lists of degree >= kBig are sorted together by one radix sort of
         // (list index, id) keys and only the prefix of short lists goes through the
         // segmented sort.
-        constexpr int64_t kBig = 8192;
+        const int64_t kBig = knobs().bigsort_min;
         int64_t nbig = 0, split = nnz;
         if (knobs().bigsort && knobs().order == 0 && g.max_degree >= kBig) {
             DevBuf<int64_t> hv;
